@@ -1,0 +1,192 @@
+/*
+ * multisplit_oracle.c -- plain, slow, obviously-correct CPU oracle for the
+ * stable multisplit of arXiv 1701.01189 ("GPU Multisplit: an extended study of
+ * a parallel algorithm", Ashkiani, Davidson, Meyer, Owens).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA path
+ * (paper_1701_01189_b200/csrc); neither side includes or links the other.
+ *
+ * Citations: "P:nnn" = line of /root/reference/PAPER.md (LaTeX source).
+ *
+ *   orc_bucket          bucket identifiers: delta f(u)=floor(u/Delta)
+ *                       (Sec.6 "Bucket identification"), identity
+ *                       f(u)=u, radix digit
+ *                       f_k(u)=(u>>kr)&(2^r-1) (Sec.7.1).
+ *                       Delta clamps to m-1 (reading R7);
+ *                       identity with u>=m is a domain error (reading R8).
+ *   orc_multisplit      stable multisplit = Eq.(1) (Sec.4.2):
+ *                       p(i) = sum_{k<j} h_k + |{u_r in B_j : r < i}|,
+ *                       computed as count -> exclusive scan -> stable
+ *                       ascending scatter.  bucket_offsets has m+1 entries
+ *                       (reading R2).
+ *   orc_tile_histogram  the matrix H=[h_{j,l}] of Eq.(2) (Sec.4.3)
+ *                       for L contiguous subproblems of T elements (last one
+ *                       ragged), stored tile-major H[l*m + j].
+ *   orc_global_scan     G = exclusive scan of row-vectorized H (P:291, P:777,
+ *                       Alg.1 P:804-812 with the index typo read as i*L+j,
+ *                       reading R3), returned in the same tile-major storage.
+ *   orc_radix_sort      the result of multisplit-sort (Sec.7.1):
+ *                       a stable sort of (keys,values) by the key bits
+ *                       [begin_bit, end_bit) as unsigned integers, written as
+ *                       a plain stable merge sort (the plain definition of
+ *                       what LSD stable passes produce, reading R10).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { ORC_OK = 0, ORC_ERR_INVALID = 1, ORC_ERR_UNSUPPORTED = 2,
+       ORC_ERR_KEY_DOMAIN = 5 };
+enum { ORC_IDENTITY = 0, ORC_DELTA = 1, ORC_RADIX = 2 };
+
+/* Validation rules of the bucket function. */
+int orc_validate(uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+                 uint32_t bits) {
+  if (m < 1 || m > 256) return ORC_ERR_UNSUPPORTED;  /* paper scope m<=256 */
+  if (kind == ORC_IDENTITY) return ORC_OK;
+  if (kind == ORC_DELTA) return delta >= 1 ? ORC_OK : ORC_ERR_INVALID;
+  if (kind == ORC_RADIX) {
+    if (bits < 1 || bits > 8) return ORC_ERR_INVALID;
+    if ((uint64_t)shift + bits > 32) return ORC_ERR_INVALID;
+    if (m != (1u << bits)) return ORC_ERR_INVALID;
+    return ORC_OK;
+  }
+  return ORC_ERR_INVALID;
+}
+
+/* Bucket identifier f(u).  Returns ORC_OK and *b in [0,m), or
+ * ORC_ERR_KEY_DOMAIN for an identity key outside [0,m). */
+int orc_bucket(uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+               uint32_t bits, uint32_t u, uint32_t *b) {
+  if (kind == ORC_IDENTITY) {             /* f(u) = u */
+    if (u >= m) return ORC_ERR_KEY_DOMAIN;
+    *b = u;
+    return ORC_OK;
+  }
+  if (kind == ORC_DELTA) {                /* f(u) = floor(u/D) */
+    uint64_t q = (uint64_t)u / delta;     /* exact 64-bit integer division */
+    *b = q < (uint64_t)(m - 1) ? (uint32_t)q : m - 1;
+    return ORC_OK;
+  }
+  /* f_k(u) = (u >> kr) & (2^r - 1) */
+  *b = (uint32_t)(((uint64_t)u >> shift) & ((1u << bits) - 1u));
+  return ORC_OK;
+}
+
+/* Eq.(1): count, exclusive scan, stable scatter.  vals_in / vals_out may be
+ * NULL (key-only).  offsets (m+1 entries) may be NULL. */
+int orc_multisplit(const uint32_t *keys_in, const uint32_t *vals_in,
+                   uint32_t *keys_out, uint32_t *vals_out, uint64_t n,
+                   uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+                   uint32_t bits, uint32_t *offsets) {
+  int st = orc_validate(kind, m, delta, shift, bits);
+  if (st) return st;
+  uint64_t h[256], cur[256];
+  memset(h, 0, sizeof h);
+  /* histogram h_k: reduction of each bucket's membership */
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t b;
+    st = orc_bucket(kind, m, delta, shift, bits, keys_in[i], &b);
+    if (st) return st;
+    h[b] += 1;
+  }
+  /* global offset: sum_{k<j} h_k (first term of Eq.1) */
+  uint64_t run = 0;
+  for (uint32_t j = 0; j < m; ++j) {
+    if (offsets) offsets[j] = (uint32_t)run;
+    cur[j] = run;
+    run += h[j];
+  }
+  if (offsets) offsets[m] = (uint32_t)run;
+  /* local offset: |{u_r in B_j : r < i}| (second term of Eq.1), obtained by
+   * visiting i in ascending order */
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t b;
+    orc_bucket(kind, m, delta, shift, bits, keys_in[i], &b);
+    uint64_t p = cur[b]++;
+    keys_out[p] = keys_in[i];
+    if (vals_in && vals_out) vals_out[p] = vals_in[i];
+  }
+  return ORC_OK;
+}
+
+/* H = [h_{j,l}] of Eq.(2): per-subproblem bucket counts for L = ceil(n/T)
+ * contiguous subproblems of T elements, stored tile-major H[l*m + j]. */
+int orc_tile_histogram(const uint32_t *keys, uint64_t n, uint64_t T,
+                       uint32_t kind, uint32_t m, uint64_t delta,
+                       uint32_t shift, uint32_t bits, uint32_t *H) {
+  int st = orc_validate(kind, m, delta, shift, bits);
+  if (st) return st;
+  if (T == 0) return ORC_ERR_INVALID;
+  uint64_t L = (n + T - 1) / T;
+  memset(H, 0, (size_t)(L * m) * sizeof(uint32_t));
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t b;
+    st = orc_bucket(kind, m, delta, shift, bits, keys[i], &b);
+    if (st) return st;
+    H[(i / T) * m + b] += 1;
+  }
+  return ORC_OK;
+}
+
+/* G = exclusive scan of the row-vectorized H (rows = buckets):
+ * H_row = [H[0][0:L-1], H[1][0:L-1], ...]; G_row = exclusive_scan(H_row).
+ * Input/output in tile-major storage X[l*m + j] = X_{j,l}. */
+void orc_global_scan(const uint32_t *H, uint64_t L, uint32_t m, uint32_t *G) {
+  uint64_t run = 0;
+  for (uint32_t j = 0; j < m; ++j)          /* row j = bucket j */
+    for (uint64_t l = 0; l < L; ++l) {      /* column l = subproblem l */
+      G[l * m + j] = (uint32_t)run;
+      run += H[l * m + j];
+    }
+}
+
+/* Stable sort of indices by digit d(i) = (keys[i] >> begin) & mask:
+ * a textbook top-down merge sort (ties keep input order). */
+static uint32_t orc_digit(uint32_t u, uint32_t begin, uint32_t end) {
+  uint32_t w = end - begin;
+  uint64_t mask = (w >= 32) ? 0xFFFFFFFFull : ((1ull << w) - 1ull);
+  return (uint32_t)(((uint64_t)u >> begin) & mask);
+}
+
+static void orc_merge_sort(uint32_t *idx, uint32_t *tmp, uint64_t lo,
+                           uint64_t hi, const uint32_t *keys, uint32_t begin,
+                           uint32_t end) {
+  if (hi - lo < 2) return;
+  uint64_t mid = lo + (hi - lo) / 2;
+  orc_merge_sort(idx, tmp, lo, mid, keys, begin, end);
+  orc_merge_sort(idx, tmp, mid, hi, keys, begin, end);
+  uint64_t a = lo, b = mid, o = lo;
+  while (a < mid && b < hi) {
+    /* take from the left run unless the right element is strictly smaller:
+     * this is what keeps equal digits in input order (stability) */
+    if (orc_digit(keys[idx[b]], begin, end) < orc_digit(keys[idx[a]], begin, end))
+      tmp[o++] = idx[b++];
+    else
+      tmp[o++] = idx[a++];
+  }
+  while (a < mid) tmp[o++] = idx[a++];
+  while (b < hi) tmp[o++] = idx[b++];
+  memcpy(idx + lo, tmp + lo, (size_t)(hi - lo) * sizeof(uint32_t));
+}
+
+int orc_radix_sort(const uint32_t *keys_in, const uint32_t *vals_in,
+                   uint32_t *keys_out, uint32_t *vals_out, uint64_t n,
+                   uint32_t begin_bit, uint32_t end_bit) {
+  if (begin_bit >= end_bit || end_bit > 32) return ORC_ERR_INVALID;
+  if (n >= (1ull << 32)) return ORC_ERR_UNSUPPORTED;
+  uint32_t *idx = (uint32_t *)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
+  uint32_t *tmp = (uint32_t *)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
+  if (!idx || !tmp) { free(idx); free(tmp); return ORC_ERR_INVALID; }
+  for (uint64_t i = 0; i < n; ++i) idx[i] = (uint32_t)i;
+  orc_merge_sort(idx, tmp, 0, n, keys_in, begin_bit, end_bit);
+  for (uint64_t i = 0; i < n; ++i) {
+    keys_out[i] = keys_in[idx[i]];
+    if (vals_in && vals_out) vals_out[i] = vals_in[idx[i]];
+  }
+  free(idx);
+  free(tmp);
+  return ORC_OK;
+}
