@@ -1,0 +1,437 @@
+#!/usr/bin/env python3
+"""bench.py -- throughput of the B200 stable multisplit (arXiv 1701.01189).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload NAME] [--m M] [--no-sweep]
+
+A step is one full multisplit (prescan -> scan -> postscan, SURVEY.md §8(a)
+rows a1-a5) of one synthetic batch resident in HBM; the radix-sort workloads'
+step is one 4-pass sort (row a6).  The default workload is BASELINE.json
+configs[1], key-only multisplit of n = 2^25 uniform uint32 keys into m = 32
+delta buckets (the north_star gate "key-only multisplit at m <= 32").  L2 is
+flushed (512 MiB write, untimed) before every timed step; each step is timed
+with CUDA events on the launching stream.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain single-threaded C) on
+a bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+# workload -> (n, pairs, kind, default m, metric unit, algorithmic bytes per element)
+# Algorithmic bytes: the paper's speed-of-light accounting: keys are
+# read twice and written once (12 B), pairs 20 B; sort = 4 passes of that.
+WORKLOADS = {
+    "ms_keys": dict(n=1 << 25, pairs=False, kind="delta", m=32, unit="Gkeys/s", bpe=12,
+                    desc="key-only multisplit, n=2^25 uniform uint32, delta buckets (configs[1])"),
+    "ms_pairs": dict(n=1 << 25, pairs=True, kind="delta", m=32, unit="Gpairs/s", bpe=20,
+                     desc="key-value multisplit, n=2^25 uniform uint32, delta buckets (configs[1])"),
+    "ms_pairs_c3": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
+                        desc="key-value multisplit, n=2^27, identity buckets (configs[2])"),
+    "ms_pairs_c3_skew": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
+                             dist="skew", desc="key-value multisplit, n=2^27, identity, 90% one bucket (configs[2])"),
+    "sort_keys": dict(n=1 << 28, pairs=False, kind="sort", m=256, unit="Gkeys/s", bpe=48,
+                      desc="multisplit LSD radix sort, 2^28 uint32 keys, 4 x 8-bit (configs[3])"),
+    "sort_pairs": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80,
+                       desc="multisplit LSD radix sort, 2^28 pairs, 4 x 8-bit (configs[3])"),
+}
+SEED = 0x5EED
+
+
+def load_peaks():
+    if os.path.exists(PEAKS_PATH):
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(key):
+    if os.path.exists(TRAFFIC_PATH):
+        with open(TRAFFIC_PATH) as f:
+            return json.load(f).get(key)
+    return None
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML in a thread during the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.index = period_s, index
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+
+    _REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+                0x2: "applications_clocks_setting", 0x100: "sync_boost", 0x10: "display_clock_setting"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self._ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- our arm
+class Runner:
+    """Holds device inputs/outputs for one workload and runs one step per call."""
+
+    def __init__(self, wl: dict, m: int, dev, rank: int = 0):
+        import torch
+        import paper_1701_01189_b200 as ms
+        from gen import device as gdev
+        from gen import inputs as gen
+
+        self.torch, self.ms, self.wl, self.m = torch, ms, wl, m
+        n = wl["n"]
+        self.n = n
+        kind = wl["kind"]
+        dist = {"skew": gen.DIST_SKEW, "binomial": gen.DIST_BINOMIAL}.get(wl.get("dist"), gen.DIST_UNIFORM)
+        self.keys = torch.empty(n, dtype=torch.int32, device=dev)
+        if kind == "delta":
+            self.bucket = ms.Delta(m)
+            gdev.keys_(self.keys, SEED + rank, kind=gen.DELTA, m=m, delta=self.bucket.delta, dist=dist, alpha=0.1)
+        elif kind == "identity":
+            self.bucket = ms.Identity(m)
+            gdev.keys_(self.keys, SEED + rank, kind=gen.IDENTITY, m=m, dist=dist, alpha=0.1)
+        elif kind == "radix":
+            bits = m.bit_length() - 1
+            self.bucket = ms.Radix(0, bits)
+            gdev.keys_(self.keys, SEED + rank, kind=gen.RADIX, m=m, shift=0, bits=bits, dist=dist, alpha=0.1)
+        else:  # sort
+            self.bucket = None
+            gdev.keys_(self.keys, SEED + rank)
+        self.vals = None
+        if wl["pairs"]:
+            self.vals = torch.empty(n, dtype=torch.int32, device=dev)
+            gdev.values_(self.vals, SEED + rank, parity=False)
+        self.ko = torch.empty_like(self.keys)
+        self.vo = torch.empty_like(self.vals) if self.vals is not None else None
+        self.off = torch.empty(m + 1, dtype=torch.int32, device=dev)
+        if kind == "sort":
+            self.ws = torch.empty(ms.radix_sort_workspace_size(n, wl["pairs"]), dtype=torch.uint8, device=dev)
+        else:
+            self.ws = torch.empty(max(1, ms.workspace_size(n, m, wl["pairs"])), dtype=torch.uint8, device=dev)
+
+    def step(self, keys=None, ko=None):
+        keys = self.keys if keys is None else keys
+        ko = self.ko if ko is None else ko
+        if self.bucket is None:
+            self.ms.radix_sort(keys, self.vals, out_keys=ko, out_values=self.vo, workspace=self.ws)
+        else:
+            self.ms.multisplit(keys, self.vals, bucket=self.bucket, out_keys=ko, out_values=self.vo,
+                               out_offsets=self.off, workspace=self.ws)
+
+
+def time_steps(run: Runner, steps: int, warmup: int, flush, stage_events: bool = True):
+    """W warm-up steps, then K steps each bracketed by CUDA events (L2 flushed before each)."""
+    import ctypes
+    import torch
+    from paper_1701_01189_b200 import _lib
+
+    lib = _lib.load()
+    for _ in range(warmup):
+        flush()
+        run.step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    stage = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for st_ in stage:  # torch creates the cudaEvent lazily: force it before taking the handle
+        for e in st_:
+            e.record()
+    handles = [(ctypes.c_void_p * 4)(*[e.cuda_event for e in st]) for st in stage]
+    launches0 = lib.ms_launch_count()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush()
+        if stage_events:
+            lib.ms_set_stage_events(handles[i])
+        ev[i][0].record()
+        run.step()
+        ev[i][1].record()
+        lib.ms_set_stage_events(None)
+    torch.cuda.synchronize()
+    launches = lib.ms_launch_count() - launches0
+    times = [a.elapsed_time(b) for a, b in ev]
+    st = None
+    if stage_events and run.bucket is not None:
+        st = {
+            "prescan": sum(s[0].elapsed_time(s[1]) for s in stage) / steps,
+            "scan": sum(s[1].elapsed_time(s[2]) for s in stage) / steps,
+            "postscan": sum(s[2].elapsed_time(s[3]) for s in stage) / steps,
+        }
+    return times, st, launches
+
+
+def e2e_steps(run: Runner, steps: int, warmup: int):
+    """Same metric through the public API with HOST buffers: pinned H2D of the inputs, the
+    multisplit / sort, D2H of the outputs (and offsets), all inside the timed region."""
+    import torch
+    n = run.n
+    kh = run.keys.cpu().pin_memory()
+    vh = run.vals.cpu().pin_memory() if run.vals is not None else None
+    koh = torch.empty(n, dtype=torch.int32).pin_memory()
+    voh = torch.empty(n, dtype=torch.int32).pin_memory() if vh is not None else None
+    kd = torch.empty_like(run.keys)
+    vd = torch.empty_like(run.vals) if run.vals is not None else None
+    h2d = 4 * n * (2 if vh is not None else 1)
+    d2h = 4 * n * (2 if vh is not None else 1) + (4 * (run.m + 1) if run.bucket is not None else 0)
+
+    def one():
+        kd.copy_(kh, non_blocking=True)
+        if vd is not None:
+            vd.copy_(vh, non_blocking=True)
+        saved = run.vals
+        run.vals = vd
+        run.step(keys=kd)
+        run.vals = saved
+        koh.copy_(run.ko, non_blocking=True)
+        if voh is not None:
+            voh.copy_(run.vo, non_blocking=True)
+        if run.bucket is not None:
+            run.off.cpu()
+
+    for _ in range(max(1, warmup)):
+        one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        one()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps, h2d, d2h
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS[args.workload]
+    m = args.m or wl["m"]
+    hbm, peak_src = load_peaks()
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    from gen import device as gdev
+    flush = lambda: gdev.flush_(scratch)  # noqa: E731
+
+    run = Runner(wl, m, dev, rank)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        times, stages, launches = time_steps(run, args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_step = sum(times) / len(times)
+    if world > 1:  # max over ranks of the device-timed step
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    n = run.n
+    value = n * world / (ms_step * 1e-3) / 1e9
+    # dominant kernel = postscan (KS); algorithmic bytes per launch: read + write of keys (+ values)
+    roofline = None
+    if stages is not None:
+        ks_bytes = n * (16 if wl["pairs"] else 8)
+        achieved = ks_bytes / (stages["postscan"] * 1e-3) / 1e9
+        roofline = {"kernel": "ks_postscan", "bound": "hbm", "achieved": round(achieved, 1),
+                    "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                    "traffic": load_traffic(f"{args.workload}_m{m}"),
+                    "alg_bytes_per_launch": ks_bytes, "peak_source": peak_src,
+                    "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
+    whole_frac = value * 1e9 / world * wl["bpe"] / (hbm * 1e9)
+    e2e_ms, h2d, d2h = e2e_steps(run, max(3, args.steps // 4), 2)
+    out = {
+        "metric": f"multisplit {wl['unit']} ({args.workload}, m={m})" if wl["kind"] != "sort"
+        else f"radix sort {wl['unit']} ({args.workload})",
+        "value": round(value, 3), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded counter-based generator)",
+        "config": {"workload": wl["desc"], "n": n, "m": m, "bucket": wl["kind"],
+                   "pairs": wl["pairs"], "l2": "flushed before every timed step (512 MiB write)",
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "hbm_roofline_frac_whole_op": round(whole_frac, 4),
+        "roofline": roofline,
+        "e2e": {"value": round(n * world / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl["unit"],
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_sweep:
+        out["sweep"] = sweep(args, dev, flush, hbm)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, m)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sweep(args, dev, flush, hbm):
+    """Per-m throughput table (BASELINE.md §2 layout), a few steps each."""
+    import torch
+    res = {}
+    cases = [("ms_keys", m) for m in (2, 8, 32, 64, 256)] + [("ms_pairs", m) for m in (2, 8, 32, 256)] + \
+            [("ms_pairs_c3", 64), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256), ("sort_keys", 256),
+             ("sort_pairs", 256)]
+    for name, m in cases:
+        wl = WORKLOADS[name]
+        run = Runner(wl, m, dev)
+        steps = 5 if wl["kind"] == "sort" else 10
+        times, stages, _ = time_steps(run, steps, 3, flush)
+        t = sum(times) / len(times)
+        rate = wl["n"] / (t * 1e-3) / 1e9
+        e = {"value": round(rate, 2), "unit": wl["unit"], "ms": round(t, 4),
+             "hbm_frac": round(rate * 1e9 * wl["bpe"] / (hbm * 1e9), 3)}
+        if stages:
+            e["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
+        res[f"{name}_m{m}"] = e
+        del run
+        torch.cuda.empty_cache()
+    return res
+
+
+# --------------------------------------------------------------------------- oracle (CPU) arm
+def _oracle_sample(wl, m, n_sample):
+    import numpy as np
+    import oracle
+    from gen import inputs as gen
+    kind = wl["kind"]
+    dist = {"skew": gen.DIST_SKEW}.get(wl.get("dist"), gen.DIST_UNIFORM)
+    if kind == "delta":
+        fn = oracle.delta(m)
+        k = gen.keys(n_sample, SEED, kind=gen.DELTA, m=m, delta=fn.delta, dist=dist, alpha=0.1)
+    elif kind == "identity":
+        fn = oracle.identity(m)
+        k = gen.keys(n_sample, SEED, kind=gen.IDENTITY, m=m, dist=dist, alpha=0.1)
+    else:
+        fn = None
+        k = gen.keys(n_sample, SEED)
+    v = gen.values(n_sample, SEED, parity=False) if wl["pairs"] else None
+    if fn is None:
+        return lambda: oracle.radix_sort(k, v)
+    return lambda: oracle.multisplit(k, fn, v)
+
+
+def cpu_baseline(wl, m, budget_s: float = 12.0):
+    """The oracle as it stands (single-threaded C) on the host, bounded sample."""
+    n_sample = min(wl["n"], 1 << 25) if wl["kind"] != "sort" else (1 << 22)
+    f = _oracle_sample(wl, m, n_sample)
+    f()
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        f()
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(n_sample / dt / 1e9, 4), "unit": wl["unit"], "cores": 1, "kind": "oracle",
+            "sample": f"{reps} x {n_sample} elements of the same workload (seed {SEED})",
+            "host_cores_available": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    m = args.m or wl["m"]
+    n_sample = min(wl["n"], 1 << 24) if wl["kind"] != "sort" else (1 << 21)
+    f = _oracle_sample(wl, m, n_sample)
+    for _ in range(args.warmup):
+        f()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        f()
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
+    value = n_sample / dt / 1e9
+    out = {"impl": "reference",
+           "metric": f"multisplit {wl['unit']} ({args.workload}, m={m})" if wl["kind"] != "sort"
+           else f"radix sort {wl['unit']} ({args.workload})",
+           "value": round(value, 4), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded counter-based generator)",
+           "config": {"workload": wl["desc"], "n": wl["n"], "m": m, "bucket": wl["kind"], "pairs": wl["pairs"]},
+           "cpu_baseline": {"value": round(value, 4), "unit": wl["unit"], "cores": 1, "kind": "oracle",
+                            "sample": f"each step: {n_sample} elements of the workload (seed {SEED})"},
+           "e2e": {"value": round(value, 4), "unit": wl["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="ms_keys")
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

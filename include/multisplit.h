@@ -1,0 +1,171 @@
+/*
+ * multisplit.h -- C ABI of libms, a B200 (sm_100a) implementation of the
+ * stable multisplit and multisplit radix sort of arXiv 1701.01189
+ * ("GPU Multisplit: an extended study of a parallel algorithm").
+ *
+ * Citations "P:nnn" are lines of the paper's LaTeX source.
+ *
+ * Conventions (all entry points):
+ *  - Data pointers are DEVICE pointers unless stated; keys and values are
+ *    32-bit words (keys unsigned, values opaque payload).
+ *  - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream).  No call allocates
+ *    memory, synchronizes, or copies to the host, except ms_device_status.
+ *  - The caller owns every buffer.  Workspace is queried with the matching
+ *    *_workspace_size function and passed in; one workspace serves one
+ *    in-flight call.  Inputs are never modified.  Outputs must not alias
+ *    inputs (P:785-787 key_in / key_out are distinct).
+ *  - Host-detectable argument errors return before anything is launched.
+ *    Device-detected key-domain errors (identity bucket with key >= m) set
+ *    a flag in the workspace that ms_device_status reports; the output of
+ *    that call is then unspecified (no out-of-bounds write happens).
+ *  - n < 2^32 (offsets are 32-bit).  1 <= m <= 256 (paper scope).
+ */
+#ifndef MULTISPLIT_H_
+#define MULTISPLIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MS_SUCCESS = 0,
+  MS_ERR_INVALID_VALUE = 1, /* null pointer, aliasing, bad bucket parameters */
+  MS_ERR_UNSUPPORTED = 2,   /* m outside [1,256], n >= 2^32 */
+  MS_ERR_WORKSPACE = 3,     /* ws_bytes smaller than the *_workspace_size value */
+  MS_ERR_CUDA = 4,          /* a CUDA launch / runtime error */
+  MS_ERR_KEY_DOMAIN = 5,    /* device-detected: identity key >= m */
+  MS_ERR_NCCL = 6           /* reserved for the sharded path */
+} ms_status;
+
+/* Bucket identifiers f(u). */
+typedef enum {
+  MS_BUCKET_IDENTITY = 0, /* f(u) = u; requires u < m                     */
+  MS_BUCKET_DELTA = 1,    /* f(u) = min(floor(u / delta), m-1), delta >= 1 */
+  MS_BUCKET_RADIX = 2     /* f(u) = (u >> shift) & (2^bits - 1), m = 2^bits */
+} ms_bucket_kind;
+
+typedef struct {
+  uint32_t kind;        /* ms_bucket_kind */
+  uint32_t num_buckets; /* m, 1..256 */
+  uint32_t delta;       /* DELTA only: bucket width, >= 1 */
+  uint32_t shift;       /* RADIX only: first bit of the digit */
+  uint32_t bits;        /* RADIX only: digit width 1..8, shift + bits <= 32 */
+} ms_bucket_fn;
+
+/* Human-readable name of a status code (static storage). */
+const char *ms_status_string(ms_status s);
+
+/* Library version, e.g. "0.1.0". */
+const char *ms_version(void);
+
+/* Fill *out with delta buckets of width ceil(2^32 / m) (2^32-1 for m = 1),
+ * the equal-width partition of the key domain of P:1107. */
+ms_status ms_bucket_delta_default(uint32_t m, ms_bucket_fn *out);
+ms_status ms_bucket_identity(uint32_t m, ms_bucket_fn *out);
+ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out);
+
+/* Check a bucket function (host only): MS_SUCCESS, MS_ERR_INVALID_VALUE or
+ * MS_ERR_UNSUPPORTED. */
+ms_status ms_bucket_validate(const ms_bucket_fn *fn);
+
+/* ------------------------------------------------------------------------
+ * Stable multisplit (Eq.(1)): permute n keys (and
+ * values) so that buckets B_0..B_{m-1} are contiguous in ascending bucket
+ * order and input order is preserved inside each bucket.
+ *
+ *   keys_in, vals_in     n words each (device).  vals_* may be NULL only in
+ *                        the _keys variant.
+ *   keys_out, vals_out   n words each (device), must not overlap the inputs.
+ *   bucket_offsets       NULL, or m+1 words (device): start of each bucket in
+ *                        the output, bucket_offsets[m] = n (reading R2).
+ *   ws, ws_bytes         device workspace of at least
+ *                        ms_multisplit_workspace_size(n, m, with_values) bytes.
+ *
+ * Pipeline (Alg.1): per-tile histogram -> global
+ * exclusive scan of the bucket x tile matrix (Eq.2) -> tile-local stable
+ * reorder in shared memory + coalesced scatter.  n <= one tile runs as a
+ * single launch.
+ * --------------------------------------------------------------------- */
+size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values);
+
+ms_status ms_multisplit_keys(const uint32_t *keys_in, uint32_t *keys_out, uint64_t n,
+                             const ms_bucket_fn *fn, uint32_t *bucket_offsets, void *ws,
+                             size_t ws_bytes, void *stream);
+
+ms_status ms_multisplit_pairs(const uint32_t *keys_in, const uint32_t *vals_in,
+                              uint32_t *keys_out, uint32_t *vals_out, uint64_t n,
+                              const ms_bucket_fn *fn, uint32_t *bucket_offsets, void *ws,
+                              size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Multisplit radix sort (Sec.7.1): ceil((end_bit-begin_bit) /
+ * bits_per_pass) LSD passes of stable multisplit with radix-digit buckets,
+ * the last pass narrower.  Result: keys ascending by the digit of
+ * bits [begin_bit, end_bit) as unsigned integers; pairs stably ordered.
+ *   0 <= begin_bit < end_bit <= 32, 1 <= bits_per_pass <= 8.
+ * --------------------------------------------------------------------- */
+size_t ms_radix_sort_workspace_size(uint64_t n, int with_values);
+
+ms_status ms_radix_sort_keys(const uint32_t *keys_in, uint32_t *keys_out, uint64_t n,
+                             uint32_t begin_bit, uint32_t end_bit, uint32_t bits_per_pass,
+                             void *ws, size_t ws_bytes, void *stream);
+
+ms_status ms_radix_sort_pairs(const uint32_t *keys_in, const uint32_t *vals_in,
+                              uint32_t *keys_out, uint32_t *vals_out, uint64_t n,
+                              uint32_t begin_bit, uint32_t end_bit, uint32_t bits_per_pass,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* Host-only: the LSD pass schedule (digit shifts and widths) used by
+ * ms_radix_sort_*.  Writes at most `cap` entries; returns the pass count,
+ * or -1 on invalid arguments. */
+int ms_radix_pass_schedule(uint32_t begin_bit, uint32_t end_bit, uint32_t bits_per_pass,
+                           uint32_t *shifts, uint32_t *bits, int cap);
+
+/* Synchronizes `stream` and returns MS_ERR_KEY_DOMAIN if the most recent
+ * multisplit that used `ws` saw an identity key >= m, else MS_SUCCESS. */
+ms_status ms_device_status(const void *ws, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Stage entry points (the three steps of P:529-540, exposed for per-stage
+ * tests and timing).  `tile` must equal ms_multisplit_tile_size().
+ * --------------------------------------------------------------------- */
+
+/* Elements per subproblem (tile) T used by the multi-tile path. */
+uint32_t ms_multisplit_tile_size(uint32_t m, int with_values);
+
+/* Prescan (Alg.1): H[l*m + j] = |{i in tile l : f(u_i) = j}|
+ * for the L = ceil(n/tile) tiles (H is L*m words, device, tile-major). */
+ms_status ms_stage_prescan(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn,
+                           uint32_t *H, uint32_t tile, void *stream);
+
+/* Scan (Alg.1): G = exclusive scan of the
+ * row-vectorized (bucket-major) H, written tile-major like H (G may equal H).
+ * bucket_offsets (m+1 words or NULL) receives the bucket starts and n_total.
+ * ws: ms_stage_scan_workspace_size(L, m) bytes. */
+size_t ms_stage_scan_workspace_size(uint64_t L, uint32_t m);
+ms_status ms_stage_scan(const uint32_t *H, uint32_t *G, uint64_t L, uint32_t m,
+                        uint32_t *bucket_offsets, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Instrumentation (host only, thread-local, zero cost when unset).
+ * --------------------------------------------------------------------- */
+
+/* Stage timing hooks: `events` is NULL (off) or points to 4 cudaEvent_t
+ * handles (passed as void*) that every subsequent multisplit call made by
+ * this host thread records on its stream: [0] before the prescan, [1] before
+ * the scan, [2] before the postscan, [3] after the postscan.  The single-CTA
+ * path (n <= tile) records [0]=[1]=[2] before and [3] after its one launch.
+ * The array must stay valid until hooks are cleared. */
+void ms_set_stage_events(void *const *events);
+
+/* Number of kernels this library has launched since load (all threads). */
+uint64_t ms_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MULTISPLIT_H_ */

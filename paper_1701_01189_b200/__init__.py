@@ -1,0 +1,198 @@
+"""paper_1701_01189_b200 -- stable multisplit and multisplit radix sort on B200.
+
+A thin Python binding over libms.so (include/multisplit.h).  PyTorch is used
+for device memory and streams only; every step of the path runs in the CUDA
+kernels of ``csrc/``.  Tensors are ``torch.int32`` or ``torch.uint32`` on a
+CUDA device and are read as uint32 bit patterns.
+
+    >>> import paper_1701_01189_b200 as ms
+    >>> k_out, v_out, offsets = ms.multisplit(keys, values, bucket=ms.Delta(32))
+    >>> k_sorted, v_sorted = ms.radix_sort(keys, values)
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import MultisplitError, check, ms_bucket_fn
+
+__all__ = ["Bucket", "Delta", "Identity", "Radix", "multisplit", "radix_sort", "device_status",
+           "prescan", "scan", "tile_size", "radix_pass_schedule", "workspace_size",
+           "MultisplitError"]
+
+
+@dataclass(frozen=True)
+class Bucket:
+    """A bucket identifier f(.): kind, m and its parameters."""
+    kind: int
+    m: int
+    delta: int = 0
+    shift: int = 0
+    bits: int = 0
+
+    def c(self) -> ms_bucket_fn:
+        return ms_bucket_fn(self.kind, self.m, self.delta, self.shift, self.bits)
+
+
+def Delta(m: int, delta: int | None = None) -> Bucket:
+    """Delta buckets f(u) = min(floor(u/delta), m-1); default width ceil(2^32/m)."""
+    if delta is None:
+        fn = ms_bucket_fn()
+        check(_lib.load().ms_bucket_delta_default(m, ctypes.byref(fn)), "ms_bucket_delta_default")
+        delta = fn.delta
+    return Bucket(_lib.MS_BUCKET_DELTA, m, delta=delta)
+
+
+def Identity(m: int) -> Bucket:
+    """Identity buckets f(u) = u, keys must lie in [0, m)."""
+    return Bucket(_lib.MS_BUCKET_IDENTITY, m)
+
+
+def Radix(shift: int, bits: int) -> Bucket:
+    """Radix-digit buckets f(u) = (u >> shift) & (2^bits - 1)."""
+    return Bucket(_lib.MS_BUCKET_RADIX, 1 << bits, shift=shift, bits=bits)
+
+
+def _u32view(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError(f"{name} must be int32 or uint32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def workspace_size(n: int, m: int, with_values: bool) -> int:
+    return int(_lib.load().ms_multisplit_workspace_size(n, m, int(with_values)))
+
+
+def multisplit(keys: torch.Tensor, values: torch.Tensor | None = None, bucket: Bucket | None = None,
+               *, out_keys: torch.Tensor | None = None, out_values: torch.Tensor | None = None,
+               offsets: bool = True, out_offsets: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None, stream=None):
+    """Stable multisplit (Eq.1).  Returns (keys_out, values_out|None, offsets|None)
+    where offsets has m+1 entries (bucket starts, offsets[m] = n)."""
+    if bucket is None:
+        raise ValueError("bucket is required (Delta / Identity / Radix)")
+    lib = _lib.load()
+    keys = _u32view(keys, "keys")
+    n = keys.numel()
+    pairs = values is not None
+    if pairs:
+        values = _u32view(values, "values")
+        if values.numel() != n:
+            raise ValueError("keys and values differ in length")
+    ko = out_keys if out_keys is not None else torch.empty_like(keys)
+    vo = (out_values if out_values is not None else torch.empty_like(values)) if pairs else None
+    off = out_offsets
+    if off is None and offsets:
+        off = torch.empty(bucket.m + 1, dtype=torch.int32, device=keys.device)
+    need = lib.ms_multisplit_workspace_size(n, bucket.m, int(pairs))
+    ws = workspace
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=keys.device)
+    fn = bucket.c()
+    sp = _stream_ptr(stream)
+    if pairs:
+        st = lib.ms_multisplit_pairs(keys.data_ptr(), values.data_ptr(), ko.data_ptr(), vo.data_ptr(),
+                                     n, ctypes.byref(fn), off.data_ptr() if off is not None else None,
+                                     ws.data_ptr(), ws.numel(), sp)
+    else:
+        st = lib.ms_multisplit_keys(keys.data_ptr(), ko.data_ptr(), n, ctypes.byref(fn),
+                                    off.data_ptr() if off is not None else None,
+                                    ws.data_ptr(), ws.numel(), sp)
+    check(st, "ms_multisplit_pairs" if pairs else "ms_multisplit_keys")
+    multisplit.last_workspace = ws
+    return ko, vo, off
+
+
+def device_status(workspace: torch.Tensor | None = None, stream=None) -> int:
+    """Sync and return the device-detected status of the last multisplit on `workspace`."""
+    ws = workspace if workspace is not None else getattr(multisplit, "last_workspace", None)
+    if ws is None:
+        raise ValueError("no workspace")
+    return int(_lib.load().ms_device_status(ws.data_ptr(), _stream_ptr(stream)))
+
+
+def radix_sort(keys: torch.Tensor, values: torch.Tensor | None = None, *, begin_bit: int = 0,
+               end_bit: int = 32, bits_per_pass: int = 8, out_keys: torch.Tensor | None = None,
+               out_values: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+               stream=None):
+    """LSD multisplit radix sort (Sec.7.1): stable sort by key bits [begin_bit, end_bit)."""
+    lib = _lib.load()
+    keys = _u32view(keys, "keys")
+    n = keys.numel()
+    pairs = values is not None
+    if pairs:
+        values = _u32view(values, "values")
+    ko = out_keys if out_keys is not None else torch.empty_like(keys)
+    vo = (out_values if out_values is not None else torch.empty_like(values)) if pairs else None
+    need = lib.ms_radix_sort_workspace_size(n, int(pairs))
+    ws = workspace
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=keys.device)
+    sp = _stream_ptr(stream)
+    if pairs:
+        st = lib.ms_radix_sort_pairs(keys.data_ptr(), values.data_ptr(), ko.data_ptr(), vo.data_ptr(), n,
+                                     begin_bit, end_bit, bits_per_pass, ws.data_ptr(), ws.numel(), sp)
+    else:
+        st = lib.ms_radix_sort_keys(keys.data_ptr(), ko.data_ptr(), n, begin_bit, end_bit, bits_per_pass,
+                                    ws.data_ptr(), ws.numel(), sp)
+    check(st, "ms_radix_sort_pairs" if pairs else "ms_radix_sort_keys")
+    return ko, vo
+
+
+def radix_sort_workspace_size(n: int, with_values: bool) -> int:
+    return int(_lib.load().ms_radix_sort_workspace_size(n, int(with_values)))
+
+
+def radix_pass_schedule(begin_bit: int = 0, end_bit: int = 32, bits_per_pass: int = 8):
+    """Host-only: [(shift, bits), ...] of the LSD passes."""
+    cap = 32
+    sh = (ctypes.c_uint32 * cap)()
+    bi = (ctypes.c_uint32 * cap)()
+    p = _lib.load().ms_radix_pass_schedule(begin_bit, end_bit, bits_per_pass, sh, bi, cap)
+    if p < 0:
+        raise ValueError("invalid radix pass parameters")
+    return [(sh[i], bi[i]) for i in range(p)]
+
+
+def tile_size(m: int = 256, with_values: bool = False) -> int:
+    return int(_lib.load().ms_multisplit_tile_size(m, int(with_values)))
+
+
+def prescan(keys: torch.Tensor, bucket: Bucket, stream=None) -> torch.Tensor:
+    """Stage 1: H as an [L, m] int32 tensor (tile-major), L = ceil(n / tile_size())."""
+    lib = _lib.load()
+    keys = _u32view(keys, "keys")
+    T = tile_size(bucket.m)
+    L = -(-keys.numel() // T)
+    H = torch.empty((L, bucket.m), dtype=torch.int32, device=keys.device)
+    fn = bucket.c()
+    check(lib.ms_stage_prescan(keys.data_ptr(), keys.numel(), ctypes.byref(fn), H.data_ptr(), T,
+                               _stream_ptr(stream)), "ms_stage_prescan")
+    return H
+
+
+def scan(H: torch.Tensor, stream=None):
+    """Stage 2: G = exclusive scan of row-vectorized H ([L, m] tile-major), and
+    the m+1 bucket offsets."""
+    lib = _lib.load()
+    H = _u32view(H, "H")
+    L, m = H.shape
+    G = torch.empty_like(H)
+    off = torch.empty(m + 1, dtype=torch.int32, device=H.device)
+    need = lib.ms_stage_scan_workspace_size(L, m)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=H.device)
+    check(lib.ms_stage_scan(H.data_ptr(), G.data_ptr(), L, m, off.data_ptr(), ws.data_ptr(), ws.numel(),
+                            _stream_ptr(stream)), "ms_stage_scan")
+    return G, off

@@ -1,0 +1,86 @@
+"""ctypes loader for libms.so (the C ABI declared in include/multisplit.h).
+
+Argument marshalling only.  There is no CPU fallback: if the shared library
+is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libms.so")
+
+MS_SUCCESS = 0
+MS_ERR_INVALID_VALUE = 1
+MS_ERR_UNSUPPORTED = 2
+MS_ERR_WORKSPACE = 3
+MS_ERR_CUDA = 4
+MS_ERR_KEY_DOMAIN = 5
+MS_ERR_NCCL = 6
+
+MS_BUCKET_IDENTITY = 0
+MS_BUCKET_DELTA = 1
+MS_BUCKET_RADIX = 2
+
+
+class ms_bucket_fn(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_uint32), ("num_buckets", ctypes.c_uint32),
+                ("delta", ctypes.c_uint32), ("shift", ctypes.c_uint32), ("bits", ctypes.c_uint32)]
+
+
+# (name, restype, argtypes) for every symbol include/multisplit.h declares.
+_P, _U32, _U64, _SZ, _I = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_int
+_FN = ctypes.POINTER(ms_bucket_fn)
+_U32P = ctypes.POINTER(ctypes.c_uint32)
+SIGNATURES = [
+    ("ms_status_string", ctypes.c_char_p, [_I]),
+    ("ms_version", ctypes.c_char_p, []),
+    ("ms_bucket_delta_default", _I, [_U32, _FN]),
+    ("ms_bucket_identity", _I, [_U32, _FN]),
+    ("ms_bucket_radix", _I, [_U32, _U32, _FN]),
+    ("ms_bucket_validate", _I, [_FN]),
+    ("ms_multisplit_workspace_size", _SZ, [_U64, _U32, _I]),
+    ("ms_multisplit_keys", _I, [_P, _P, _U64, _FN, _P, _P, _SZ, _P]),
+    ("ms_multisplit_pairs", _I, [_P, _P, _P, _P, _U64, _FN, _P, _P, _SZ, _P]),
+    ("ms_radix_sort_workspace_size", _SZ, [_U64, _I]),
+    ("ms_radix_sort_keys", _I, [_P, _P, _U64, _U32, _U32, _U32, _P, _SZ, _P]),
+    ("ms_radix_sort_pairs", _I, [_P, _P, _P, _P, _U64, _U32, _U32, _U32, _P, _SZ, _P]),
+    ("ms_radix_pass_schedule", _I, [_U32, _U32, _U32, _U32P, _U32P, _I]),
+    ("ms_device_status", _I, [_P, _P]),
+    ("ms_multisplit_tile_size", _U32, [_U32, _I]),
+    ("ms_stage_prescan", _I, [_P, _U64, _FN, _P, _U32, _P]),
+    ("ms_stage_scan_workspace_size", _SZ, [_U64, _U32]),
+    ("ms_stage_scan", _I, [_P, _P, _U64, _U32, _P, _P, _SZ, _P]),
+    ("ms_set_stage_events", None, [_P]),
+    ("ms_launch_count", _U64, []),
+]
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libms.so (built by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class MultisplitError(RuntimeError):
+    def __init__(self, code: int, where: str = ""):
+        name = load().ms_status_string(code).decode()
+        super().__init__(f"{where}: {name} ({code})" if where else f"{name} ({code})")
+        self.code = code
+
+
+def check(code: int, where: str = "") -> None:
+    if code != MS_SUCCESS:
+        raise MultisplitError(code, where)

@@ -1,0 +1,168 @@
+// ms_device.cuh -- device-side building blocks for the sm_100a multisplit:
+// bucket identifiers, warp-level ranking helpers and the PTX wrappers for the
+// TMA bulk-copy engine (cp.async.bulk + mbarrier) and release/acquire flags.
+//
+// Citations "P:nnn" are lines of the paper's LaTeX source.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ms {
+
+// ---------------------------------------------------------------- tunables
+constexpr int kWarp = 32;
+// Multi-tile path: one CTA per subproblem ("tile") of kTile elements.
+// 16 warps x 16 windows x 32 lanes = 8192 (B200's 227 KB smem lets the tile
+// be 8x the paper's 1024-element BMS tile, so that at m = 256 the
+// average bucket run per tile is 32 elements = 128 B of coalesced writes).
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / kWarp;
+constexpr int kItems = 16;                     // windows per warp (keys per thread)
+constexpr int kTile = kThreads * kItems;       // 8192
+constexpr int kMaxBuckets = 256;
+
+enum BucketKind : uint32_t { kIdentity = 0, kDelta = 1, kRadix = 2 };
+
+// Bucket identifier parameters, precomputed on the host.
+struct BucketParams {
+  uint32_t m;        // number of buckets
+  uint32_t m1;       // m - 1
+  uint32_t shift;    // RADIX
+  uint32_t mask;     // RADIX: 2^bits - 1
+  uint32_t magic_hi; // DELTA: M = ceil(2^64 / delta) split in two words
+  uint32_t magic_lo;
+  uint32_t delta_is_one;
+};
+
+// f(u) for the three identifiers.  DELTA computes
+// floor(u / delta) exactly as the high 64 bits of u * ceil(2^64/delta): the
+// rounding error u*e/(delta*2^64) < 2^-32 <= 1/delta never crosses an integer
+// for u, delta < 2^32.  IDENTITY clamps keys
+// >= m into m-1 (the domain error itself is flagged by the caller).
+template <int KIND>
+__device__ __forceinline__ uint32_t bucket_of(uint32_t u, const BucketParams &p) {
+  if constexpr (KIND == kRadix) {
+    return (u >> p.shift) & p.mask;
+  } else if constexpr (KIND == kIdentity) {
+    return u < p.m1 ? u : p.m1;
+  } else {
+    uint32_t q;
+    if (p.delta_is_one) {
+      q = u;
+    } else {
+      uint64_t t = (uint64_t)u * p.magic_hi + __umulhi(u, p.magic_lo);
+      q = (uint32_t)(t >> 32);
+    }
+    return q < p.m1 ? q : p.m1;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ bool key_domain_error(uint32_t u, const BucketParams &p) {
+  if constexpr (KIND == kIdentity) return u >= p.m;
+  return false;
+}
+
+// ---------------------------------------------------------------- warp helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Peer mask of Alg.3 (reading R4): the lanes of `active` whose
+// bucket equals mine, from ceil(log2 m) binary ballots of the bucket bits
+// (ballot-based voting).
+template <int LOGM>
+__device__ __forceinline__ uint32_t peer_mask_ballot(uint32_t b, uint32_t active, bool valid) {
+  uint32_t peers = active;
+#pragma unroll
+  for (int k = 0; k < LOGM; ++k) {
+    const bool bit = (b >> k) & 1u;
+    const uint32_t vote = __ballot_sync(0xFFFFFFFFu, valid && bit);
+    peers &= bit ? vote : ~vote;
+  }
+  return peers;
+}
+
+// ---------------------------------------------------------------- PTX: smem address
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- PTX: mbarrier + TMA bulk copy
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP); bytes
+// and both addresses must be multiples of 16.  Completion is signalled on
+// `bar` as transaction bytes.  L2 policy: evict_first for streamed input.
+__device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gmem_src, uint32_t bytes,
+                                            uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---------------------------------------------------------------- PTX: global loads / flags
+__device__ __forceinline__ uint4 ldg_stream_v4(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+}  // namespace ms

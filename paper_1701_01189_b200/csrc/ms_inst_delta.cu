@@ -1,0 +1,6 @@
+// Kernel instantiations for the delta bucket identifier (see ms_dispatch.cuh).
+#include "ms_dispatch.cuh"
+
+namespace ms {
+MS_INSTANTIATE_KIND(kDelta)
+}  // namespace ms

@@ -1,0 +1,6 @@
+// Kernel instantiations for the radix bucket identifier (see ms_dispatch.cuh).
+#include "ms_dispatch.cuh"
+
+namespace ms {
+MS_INSTANTIATE_KIND(kRadix)
+}  // namespace ms

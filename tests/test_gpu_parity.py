@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, on the same seeded inputs.  Integer work => bit-exact.
+
+Grid: SPEC acceptance grid m in {1,2,3,8,32,33,64,255,256} x
+n in {0,1,31,32,33,1000,2^20}, plus tile-boundary sizes (ragged tails), the
+three bucket identifiers, keys and pairs, uniform / skewed / single-bucket /
+binomial inputs; stage-level checks of H and G; radix sort; full-size
+configurations of BASELINE.json in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+ms = pytest.importorskip("paper_1701_01189_b200")
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+def bucket_pair(kind: str, m: int):
+    """(oracle bucket, product bucket, generator kwargs)"""
+    if kind == "delta":
+        o = oracle.delta(m)
+        return o, ms.Delta(m), dict(kind=gen.DELTA, m=m, delta=o.delta)
+    if kind == "identity":
+        return oracle.identity(m), ms.Identity(m), dict(kind=gen.IDENTITY, m=m)
+    bits = max(1, (m - 1).bit_length())
+    shift = 32 - bits - 3
+    return oracle.radix(shift, bits), ms.Radix(shift, bits), dict(kind=gen.RADIX, m=1 << bits,
+                                                                     shift=shift, bits=bits)
+
+
+def check_multisplit(keys, vals, ob, pb):
+    ek, ev, eo = oracle.multisplit(keys, ob, vals)
+    ko, vo, off = ms.multisplit(dev(keys), None if vals is None else dev(vals), bucket=pb)
+    assert np.array_equal(host(ko), ek), "keys differ"
+    if vals is not None:
+        assert np.array_equal(host(vo), ev), "values differ"
+    assert np.array_equal(host(off), eo), "bucket offsets differ"
+    assert ms.device_status() == 0
+
+
+GRID_M = [1, 2, 3, 8, 32, 33, 64, 255, 256]
+GRID_N = [0, 1, 31, 32, 33, 1000, 1 << 20]
+
+
+@pytest.mark.parametrize("m", GRID_M)
+@pytest.mark.parametrize("n", GRID_N)
+@pytest.mark.parametrize("pairs", [False, True])
+def test_spec_grid_delta(m, n, pairs):
+    ob, pb, gk = bucket_pair("delta", m)
+    keys = gen.keys(n, seed=1 + m, **gk)
+    check_multisplit(keys, gen.values(n, seed=1) if pairs else None, ob, pb)
+
+
+@pytest.mark.parametrize("kind", ["identity", "radix"])
+@pytest.mark.parametrize("m", GRID_M)
+@pytest.mark.parametrize("n", [33, 1000, 1 << 20])
+def test_spec_grid_identity_radix(kind, m, n):
+    if kind == "radix" and m == 1:
+        pytest.skip("radix digits have m = 2^bits >= 2")
+    ob, pb, gk = bucket_pair(kind, m)
+    keys = gen.keys(n, seed=2, dist=gen.DIST_UNIFORM, **gk)
+    check_multisplit(keys, gen.values(n, seed=2), ob, pb)
+
+
+T = 8192  # ms.tile_size(); checked below
+
+
+def test_tile_size():
+    assert ms.tile_size() == T
+
+
+@pytest.mark.parametrize("n", [T - 1, T, T + 1, 2 * T - 3, 3 * T + 5, 37 * T + 4097])
+@pytest.mark.parametrize("m", [2, 5, 32, 200, 256])
+@pytest.mark.parametrize("dist", [gen.DIST_UNIFORM, gen.DIST_SKEW, gen.DIST_BINOMIAL])
+def test_tile_boundaries_and_distributions(n, m, dist):
+    ob, pb, gk = bucket_pair("delta", m)
+    keys = gen.keys(n, seed=n, dist=dist, alpha=0.1, **gk)
+    check_multisplit(keys, gen.values(n, seed=3), ob, pb)
+
+
+@pytest.mark.parametrize("m", [2, 17, 256])
+def test_single_bucket_is_copy(m):
+    ob, pb, gk = bucket_pair("identity", m)
+    n = 5 * T + 123
+    keys = gen.keys(n, seed=4, dist=gen.DIST_SKEW, alpha=0.0, **gk)
+    vals = gen.values(n, seed=4, parity=False)
+    ko, vo, off = ms.multisplit(dev(keys), dev(vals), bucket=pb)
+    assert np.array_equal(host(ko), keys) and np.array_equal(host(vo), vals)
+    check_multisplit(keys, vals, ob, pb)
+
+
+@pytest.mark.parametrize("kind", ["delta", "identity", "radix"])
+def test_unaligned_inputs(kind):
+    # inputs not 16-byte aligned take the non-TMA load path
+    ob, pb, gk = bucket_pair(kind, 37)
+    n = 3 * T + 11
+    keys = gen.keys(n + 1, seed=5, **gk)
+    vals = gen.values(n + 1, seed=5)
+    kd, vd = dev(keys), dev(vals)
+    ko, vo, off = ms.multisplit(kd[1:], vd[1:], bucket=pb)
+    ek, ev, eo = oracle.multisplit(keys[1:], ob, vals[1:])
+    assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev)
+    assert np.array_equal(host(off), eo)
+
+
+def test_custom_delta_widths():
+    for m, d in ((7, 1), (7, 3), (100, 12345), (256, 2**24 + 7), (3, 2**31 + 1)):
+        ob, pb = oracle.delta(m, d), ms.Delta(m, d)
+        keys = gen.keys(3 * T + 1, seed=d % 1000)
+        keys[:64] = np.array([0, 1, d - 1, d, d + 1, m * d - 1, m * d, 0xFFFFFFFF] * 8, np.uint64).astype(np.uint32)
+        check_multisplit(keys, gen.values(keys.size, seed=1), ob, pb)
+
+
+@pytest.mark.parametrize("n", [100, 3 * T + 7])
+def test_identity_domain_error_flag(n):
+    keys = gen.keys(n, seed=6, kind=gen.IDENTITY, m=8)
+    _, _, _ = ms.multisplit(dev(keys), bucket=ms.Identity(8))
+    assert ms.device_status() == 0
+    keys[n // 2] = 8
+    ko, _, _ = ms.multisplit(dev(keys), bucket=ms.Identity(8))
+    assert ms.device_status() == 5  # MS_ERR_KEY_DOMAIN
+    ms.multisplit(dev(keys % 8), bucket=ms.Identity(8))
+    assert ms.device_status() == 0  # the flag belongs to the most recent call
+
+
+# ------------------------------------------------------------------ stages (H, G)
+
+@pytest.mark.parametrize("m", [1, 2, 8, 33, 256])
+@pytest.mark.parametrize("n", [1, T, 5 * T + 77])
+def test_stage_prescan(m, n):
+    ob, pb, gk = bucket_pair("delta", m)
+    keys = gen.keys(n, seed=7, dist=gen.DIST_BINOMIAL, **gk)
+    H = ms.prescan(dev(keys), pb)
+    assert np.array_equal(host(H), oracle.tile_histogram(keys, ob, T))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 256), (4096, 2), (4096, 32), (2049, 33), (32768, 256), (5, 255)])
+def test_stage_scan(shape):
+    L, m = shape
+    rng = np.random.default_rng(L * m)
+    Hn = rng.integers(0, 60, shape, dtype=np.uint64).astype(np.uint32)
+    G, off = ms.scan(dev(Hn))
+    eG = oracle.global_scan(Hn)
+    assert np.array_equal(host(G), eG)
+    tot = Hn.astype(np.int64).sum(axis=0)
+    assert np.array_equal(host(off).astype(np.int64), np.concatenate([[0], np.cumsum(tot)]))
+
+
+# ------------------------------------------------------------------ radix sort (Sec.7.1)
+
+@pytest.mark.parametrize("n", [0, 1, 1000, T, 4 * T + 9, 1 << 20])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_radix_sort(n, pairs):
+    keys = gen.keys(n, seed=9)
+    keys[::5] &= np.uint32(0xFF00FF)  # duplicates make stability visible
+    vals = gen.values(n, seed=9)
+    ek, ev = oracle.radix_sort(keys, vals if pairs else None)
+    ko, vo = ms.radix_sort(dev(keys), dev(vals) if pairs else None)
+    assert np.array_equal(host(ko), ek)
+    if pairs:
+        assert np.array_equal(host(vo), ev)
+
+
+@pytest.mark.parametrize("args", [(0, 32, 4), (0, 32, 7), (0, 32, 5), (8, 24, 8), (3, 17, 6), (31, 32, 1)])
+def test_radix_sort_bits(args):
+    b0, b1, r = args
+    n = 3 * T + 100
+    keys = gen.keys(n, seed=b1)
+    vals = gen.values(n, seed=1)
+    ek, ev = oracle.radix_sort(keys, vals, b0, b1)
+    ko, vo = ms.radix_sort(dev(keys), dev(vals), begin_bit=b0, end_bit=b1, bits_per_pass=r)
+    assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev)
+
+
+def test_determinism_repeated_runs():
+    n, m = 40 * T + 17, 64
+    ob, pb, gk = bucket_pair("delta", m)
+    keys = dev(gen.keys(n, seed=10, dist=gen.DIST_SKEW, **gk))
+    vals = dev(gen.values(n, seed=10))
+    ref = ms.multisplit(keys, vals, bucket=pb)
+    for _ in range(20):
+        out = ms.multisplit(keys, vals, bucket=pb)
+        for a, b in zip(ref, out):
+            assert torch.equal(a, b)
