@@ -131,14 +131,16 @@ ms_status ms_device_status(const void *ws, void *stream);
 
 /* ------------------------------------------------------------------------
  * Stage entry points (the three steps of P:529-540, exposed for per-stage
- * tests and timing).  `tile` must equal ms_multisplit_tile_size().
+ * tests and timing).
  * --------------------------------------------------------------------- */
 
-/* Elements per subproblem (tile) T used by the multi-tile path. */
+/* Elements per tile T (the subproblem reordered in shared memory) used by
+ * the product path: 8192 for keys, 4096 for pairs. */
 uint32_t ms_multisplit_tile_size(uint32_t m, int with_values);
 
 /* Prescan (Alg.1): H[l*m + j] = |{i in tile l : f(u_i) = j}|
- * for the L = ceil(n/tile) tiles (H is L*m words, device, tile-major). */
+ * for the L = ceil(n/tile) subproblems of `tile` (>= 1) consecutive elements
+ * (H is L*m words, device, tile-major). */
 ms_status ms_stage_prescan(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn,
                            uint32_t *H, uint32_t tile, void *stream);
 

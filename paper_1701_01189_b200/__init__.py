@@ -170,11 +170,11 @@ def tile_size(m: int = 256, with_values: bool = False) -> int:
     return int(_lib.load().ms_multisplit_tile_size(m, int(with_values)))
 
 
-def prescan(keys: torch.Tensor, bucket: Bucket, stream=None) -> torch.Tensor:
-    """Stage 1: H as an [L, m] int32 tensor (tile-major), L = ceil(n / tile_size())."""
+def prescan(keys: torch.Tensor, bucket: Bucket, tile: int | None = None, stream=None) -> torch.Tensor:
+    """Stage 1: H as an [L, m] int32 tensor (tile-major), L = ceil(n / tile)."""
     lib = _lib.load()
     keys = _u32view(keys, "keys")
-    T = tile_size(bucket.m)
+    T = tile or tile_size(bucket.m)
     L = -(-keys.numel() // T)
     H = torch.empty((L, bucket.m), dtype=torch.int32, device=keys.device)
     fn = bucket.c()

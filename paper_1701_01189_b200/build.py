@@ -15,7 +15,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
 
-SOURCES = ["ms_capi.cu", "ms_inst_identity.cu", "ms_inst_delta.cu", "ms_inst_radix.cu"]
+SOURCES = ["ms_capi.cu", "ms_inst_identity.cu", "ms_inst_delta.cu", "ms_inst_radix.cu",
+           "ms_inst_deltashift.cu"]
 HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_dispatch.cuh", "ms_scan.cuh"]
 
 

@@ -10,15 +10,6 @@
 #include "ms_dispatch.cuh"
 #include "ms_scan.cuh"
 
-namespace ms {
-template <int KIND>
-cudaError_t launch_prescan(int, int, const uint32_t *, uint32_t, const BucketParams &,
-                           uint32_t *, unsigned long long *, uint32_t, uint32_t *, cudaStream_t);
-template <int KIND>
-cudaError_t launch_postscan(int, int, bool, const KsArgs &, const BucketParams &, uint32_t,
-                            cudaStream_t);
-}  // namespace ms
-
 using namespace ms;
 
 namespace {
@@ -41,37 +32,34 @@ constexpr size_t kBaseBytes = 1280; // m+1 <= 257 words
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-uint32_t ceil_log2(uint32_t m) {
-  uint32_t l = 0;
-  while ((1u << l) < m) ++l;
-  return l;
-}
-
 // tiles per look-back chunk: ~4096 H words per scan CTA
 uint32_t scan_chunk_tiles(uint32_t m) {
   uint32_t c = 4096u / m;
   return c < 1 ? 1 : c;
 }
 
+uint32_t tile_elems(bool pairs) { return pairs ? (uint32_t)kTilePairs : (uint32_t)kTileKeys; }
+
+// Workspace: [hdr 256 B][base 1280 B][R or H: L*m words][KG status: nchunks*m u64]
+// (the level-0 histogram R needs G <= L rows; the three-launch mode needs L rows of H).
 struct Layout {
   size_t base, H, status, total;
-  uint32_t L, nchunks, C;
+  uint32_t T, L, nchunks, C;
 };
 
-Layout layout_for(uint64_t n, uint32_t m) {
+Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   Layout lo{};
+  lo.T = tile_elems(pairs);
   lo.base = kHdrBytes;
-  if (n <= (uint64_t)kTile) {  // single-CTA path: header only
-    lo.H = lo.status = lo.total = kHdrBytes + kBaseBytes;
+  lo.H = kHdrBytes + kBaseBytes;
+  if (n <= lo.T) {  // single-CTA path: header only
+    lo.status = lo.total = lo.H;
     lo.L = n ? 1 : 0;
-    lo.nchunks = 0;
-    lo.C = 0;
     return lo;
   }
-  lo.L = (uint32_t)((n + kTile - 1) / kTile);
+  lo.L = (uint32_t)((n + lo.T - 1) / lo.T);
   lo.C = scan_chunk_tiles(m);
   lo.nchunks = (lo.L + lo.C - 1) / lo.C;
-  lo.H = kHdrBytes + kBaseBytes;
   lo.status = lo.H + align_up((size_t)lo.L * m * 4u);
   lo.total = lo.status + align_up((size_t)lo.nchunks * m * 8u);
   return lo;
@@ -93,45 +81,52 @@ ms_status validate_fn(const ms_bucket_fn *fn) {
   }
 }
 
-BucketParams make_params(const ms_bucket_fn *fn) {
-  BucketParams p{};
+// Device kind + parameters.  DELTA with delta = 2^s becomes a shift (kDeltaShift).
+struct Plan {
+  int kind;
+  BucketParams bp;
+};
+
+Plan make_plan(const ms_bucket_fn *fn) {
+  Plan pl{};
+  BucketParams &p = pl.bp;
   p.m = fn->num_buckets;
   p.m1 = fn->num_buckets - 1;
-  p.shift = fn->shift;
-  p.mask = fn->kind == MS_BUCKET_RADIX ? ((1u << fn->bits) - 1u) : 0u;
-  if (fn->kind == MS_BUCKET_DELTA) {
-    p.delta_is_one = fn->delta == 1;
-    if (!p.delta_is_one) {
-      // M = ceil(2^64 / delta) = floor((2^64 - 1) / delta) + 1  (delta >= 2)
-      const unsigned long long M = ~0ull / fn->delta + 1ull;
-      p.magic_hi = (uint32_t)(M >> 32);
-      p.magic_lo = (uint32_t)M;
+  switch (fn->kind) {
+    case MS_BUCKET_IDENTITY: pl.kind = kIdentity; break;
+    case MS_BUCKET_RADIX:
+      pl.kind = kRadix;
+      p.shift = fn->shift;
+      p.mask = (1u << fn->bits) - 1u;
+      break;
+    default: {
+      const uint32_t d = fn->delta;
+      if ((d & (d - 1u)) == 0u) {  // power of two, including delta = 1
+        pl.kind = kDeltaShift;
+        p.shift = (uint32_t)__builtin_ctz(d);
+      } else {
+        pl.kind = kDelta;
+        // M = ceil(2^64 / delta) = floor((2^64 - 1) / delta) + 1   (delta >= 3 here)
+        const unsigned long long M = ~0ull / d + 1ull;
+        p.magic_hi = (uint32_t)(M >> 32);
+        p.magic_lo = (uint32_t)M;
+      }
     }
   }
-  return p;
+  return pl;
 }
 
-int env_strategy(const char *name, int dflt) {
-  const char *v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  if (!std::strcmp(v, "count1")) return kCount1;
-  if (!std::strcmp(v, "peers") || !std::strcmp(v, "ballot")) return kPeers;
-  if (!std::strcmp(v, "match")) return kMatch;
-  if (!std::strcmp(v, "atomic")) return kAtomic;
-  return dflt;
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    return 148;
+  return n;
 }
 
-// Per-m strategy table; env overrides for the bench only.
-int hist_strategy(uint32_t m) {
-  int s = env_strategy("MS_HIST", m <= 2 ? kCount1 : kPeers);
-  if (s == kCount1 && m > 2) s = kPeers;
-  return s;
-}
-int rank_strategy(uint32_t m) {
-  int s = env_strategy("MS_RANK", m <= 2 ? kCount1 : kPeers);
-  if (s == kCount1 && m > 2) s = kPeers;
-  if (s == kAtomic) s = kPeers;
-  return s;
+bool three_launch_mode() {
+  const char *v = std::getenv("MS_PIPELINE");
+  return v && !std::strcmp(v, "3pass");
 }
 
 bool overlaps(const void *a, const void *b, uint64_t n) {
@@ -141,24 +136,32 @@ bool overlaps(const void *a, const void *b, uint64_t n) {
   return pa < pb + bytes && pb < pa + bytes;
 }
 
-cudaError_t prescan_dispatch(uint32_t kind, int strat, int logm, const uint32_t *keys, uint32_t n,
-                             const BucketParams &bp, uint32_t *H, unsigned long long *zs,
-                             uint32_t zw, uint32_t *hdr, cudaStream_t s) {
-  switch (kind) {
-    case MS_BUCKET_IDENTITY:
-      return launch_prescan<kIdentity>(strat, logm, keys, n, bp, H, zs, zw, hdr, s);
-    case MS_BUCKET_DELTA:
-      return launch_prescan<kDelta>(strat, logm, keys, n, bp, H, zs, zw, hdr, s);
-    default: return launch_prescan<kRadix>(strat, logm, keys, n, bp, H, zs, zw, hdr, s);
+cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t per,
+                       uint32_t grid, uint32_t *R, uint32_t *hdr, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
   }
 }
 
-cudaError_t postscan_dispatch(uint32_t kind, int strat, int logm, bool pairs, const KsArgs &a,
-                              const BucketParams &bp, uint32_t grid, cudaStream_t s) {
-  switch (kind) {
-    case MS_BUCKET_IDENTITY: return launch_postscan<kIdentity>(strat, logm, pairs, a, bp, grid, s);
-    case MS_BUCKET_DELTA: return launch_postscan<kDelta>(strat, logm, pairs, a, bp, grid, s);
-    default: return launch_postscan<kRadix>(strat, logm, pairs, a, bp, grid, s);
+cudaError_t tile_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t tile,
+                      uint32_t grid, uint32_t *H, uint32_t *hdr, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
+    case kDelta: return Launch<kDelta>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
+    case kRadix: return Launch<kRadix>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
+    default: return Launch<kDeltaShift>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
+  }
+}
+
+cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::fused(pairs, a, pl.bp, grid, s);
+    case kDelta: return Launch<kDelta>::fused(pairs, a, pl.bp, grid, s);
+    case kRadix: return Launch<kRadix>::fused(pairs, a, pl.bp, grid, s);
+    default: return Launch<kDeltaShift>::fused(pairs, a, pl.bp, grid, s);
   }
 }
 
@@ -179,7 +182,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
                   overlaps(vals_in, keys_out, n) || overlaps(keys_out, vals_out, n)))
       return MS_ERR_INVALID_VALUE;
   }
-  const Layout lo = layout_for(n, m);
+  const Layout lo = layout_for(n, m, pairs);
   if (ws_bytes < lo.total) return MS_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   char *w = (char *)ws;
@@ -192,10 +195,8 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
     return MS_SUCCESS;
   }
 
-  const BucketParams bp = make_params(fn);
-  const int logm = m <= 2 ? 1 : (int)ceil_log2(m);
-  const int hs = hist_strategy(m), rs = rank_strategy(m);
-  KsArgs a{};
+  const Plan pl = make_plan(fn);
+  KfArgs a{};
   a.keys_in = keys_in;
   a.vals_in = pairs ? vals_in : nullptr;
   a.keys_out = keys_out;
@@ -205,32 +206,58 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.bucket_offsets = bucket_offsets;
   a.use_tma = (((uintptr_t)keys_in & 15u) == 0) && (!pairs || (((uintptr_t)vals_in & 15u) == 0));
 
-  if (n <= (uint64_t)kTile) {  // one subproblem: a single fused launch
-    a.single = 1;
+  if (n <= lo.T) {  // one subproblem: a single launch
+    a.mode = kModeSingle;
+    a.num_tiles = 1;
+    a.tiles_per_cta = 1;
     stage_event(0, s);
     stage_event(1, s);
     stage_event(2, s);
-    const cudaError_t e = counted(postscan_dispatch(fn->kind, rs, logm, pairs, a, bp, 1, s));
+    const cudaError_t e = counted(fused(pl, pairs, a, 1, s));
     stage_event(3, s);
     return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
   }
 
   uint32_t *base = (uint32_t *)(w + lo.base);
   uint32_t *H = (uint32_t *)(w + lo.H);
-  unsigned long long *status = (unsigned long long *)(w + lo.status);
+  a.num_tiles = lo.L;
+
+  if (three_launch_mode()) {
+    // paper-faithful {local, global, local}: tile histograms H -> scan -> postscan
+    unsigned long long *status = (unsigned long long *)(w + lo.status);
+    stage_event(0, s);
+    if (counted(tile_hist(pl, keys_in, (uint32_t)n, lo.T, lo.L, H, hdr, s)) != cudaSuccess)
+      return MS_ERR_CUDA;
+    stage_event(1, s);
+    zero_words_kernel<<<64, 256, 0, s>>>(status, lo.nchunks * m, hdr + 1);
+    kg_scan<<<lo.nchunks, kScanThreads, 0, s>>>(H, H, lo.L, m, lo.C, lo.nchunks, status,
+                                                 hdr + 1, base, bucket_offsets);
+    if (counted(cudaGetLastError(), 2) != cudaSuccess) return MS_ERR_CUDA;
+    stage_event(2, s);
+    a.mode = kModeTileG;
+    a.Gt = H;
+    a.base = base;
+    a.tiles_per_cta = 1;
+    a.num_ranges = lo.L;
+    const cudaError_t e = counted(fused(pl, pairs, a, lo.L, s));
+    stage_event(3, s);
+    return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+  }
+
+  // level-0 localization: G ranges of K consecutive tiles (2 CTAs per SM)
+  const uint32_t target = (uint32_t)sm_count() * 2u;
+  const uint32_t K = (lo.L + target - 1) / target;
+  const uint32_t G = (lo.L + K - 1) / K;
   stage_event(0, s);
-  if (counted(prescan_dispatch(fn->kind, hs, logm, keys_in, (uint32_t)n, bp, H, status,
-                               lo.nchunks * m, hdr, s)) != cudaSuccess)
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
-  kg_scan<<<lo.nchunks, kScanThreads, 0, s>>>(H, H, lo.L, m, lo.C, lo.nchunks, status, hdr + 1,
-                                               base, bucket_offsets);
-  if (counted(cudaGetLastError()) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
-  a.single = 0;
-  a.G = H;
-  a.base = base;
-  const cudaError_t e = counted(postscan_dispatch(fn->kind, rs, logm, pairs, a, bp, lo.L, s));
+  a.mode = kModeRange;
+  a.R = H;
+  a.tiles_per_cta = K;
+  a.num_ranges = G;
+  const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
 }
@@ -314,10 +341,9 @@ ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out) {
 ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn); }
 
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
-  (void)with_values;
   if (m < 1) m = 1;
   if (m > 256) m = 256;
-  return layout_for(n, m).total;
+  return layout_for(n, m, with_values != 0).total;
 }
 
 ms_status ms_multisplit_keys(const uint32_t *keys_in, uint32_t *keys_out, uint64_t n,
@@ -379,23 +405,21 @@ ms_status ms_device_status(const void *ws, void *stream) {
 
 uint32_t ms_multisplit_tile_size(uint32_t m, int with_values) {
   (void)m;
-  (void)with_values;
-  return (uint32_t)kTile;
+  return tile_elems(with_values != 0);
 }
 
 ms_status ms_stage_prescan(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn,
                            uint32_t *H, uint32_t tile, void *stream) {
   ms_status st = validate_fn(fn);
   if (st != MS_SUCCESS) return st;
-  if (tile != (uint32_t)kTile) return MS_ERR_INVALID_VALUE;
+  if (tile == 0) return MS_ERR_INVALID_VALUE;
   if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
   if (n == 0) return MS_SUCCESS;
   if (!keys_in || !H) return MS_ERR_INVALID_VALUE;
-  const uint32_t m = fn->num_buckets;
-  const BucketParams bp = make_params(fn);
-  const int logm = m <= 2 ? 1 : (int)ceil_log2(m);
-  return counted(prescan_dispatch(fn->kind, hist_strategy(m), logm, keys_in, (uint32_t)n, bp, H,
-                                  nullptr, 0, nullptr, (cudaStream_t)stream)) == cudaSuccess
+  const Plan pl = make_plan(fn);
+  const uint32_t L = (uint32_t)((n + tile - 1) / tile);
+  return counted(tile_hist(pl, keys_in, (uint32_t)n, tile, L, H, nullptr,
+                           (cudaStream_t)stream)) == cudaSuccess
              ? MS_SUCCESS
              : MS_ERR_CUDA;
 }

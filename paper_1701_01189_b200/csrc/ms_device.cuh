@@ -11,17 +11,27 @@ namespace ms {
 
 // ---------------------------------------------------------------- tunables
 constexpr int kWarp = 32;
-// Multi-tile path: one CTA per subproblem ("tile") of kTile elements.
-// 16 warps x 16 windows x 32 lanes = 8192 (B200's 227 KB smem lets the tile
-// be 8x the paper's 1024-element BMS tile, so that at m = 256 the
-// average bucket run per tile is 32 elements = 128 B of coalesced writes).
+// One CTA = 16 warps.  A tile (the subproblem of the last localization level
+// reordered in shared memory) is 16 windows x 32 lanes per warp
+// for keys (8192 elements) and 8 windows per warp for pairs (4096): 32 KB of
+// keys either way.  B200's 227 KB of shared memory lets a tile be 8x the
+// paper's 1024-element BMS tile, so that at m = 256 the average
+// bucket run per key tile is 32 elements = 128 B of coalesced writes.
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
-constexpr int kItems = 16;                     // windows per warp (keys per thread)
-constexpr int kTile = kThreads * kItems;       // 8192
 constexpr int kMaxBuckets = 256;
 
-enum BucketKind : uint32_t { kIdentity = 0, kDelta = 1, kRadix = 2 };
+template <bool PAIRS>
+struct TileCfg {
+  static constexpr int kItems = PAIRS ? 8 : 16;  // windows per warp = elements per thread
+  static constexpr int kTile = kThreads * kItems;
+};
+constexpr int kTileKeys = TileCfg<false>::kTile;    // 8192
+constexpr int kTilePairs = TileCfg<true>::kTile;    // 4096
+
+// kDeltaShift is the internal form of DELTA when delta = 2^shift: floor(u/delta)
+// is a shift (the bench's equal-width buckets of P:1107 with m = 2^k).
+enum BucketKind : uint32_t { kIdentity = 0, kDelta = 1, kRadix = 2, kDeltaShift = 3 };
 
 // Bucket identifier parameters, precomputed on the host.
 struct BucketParams {
@@ -43,6 +53,9 @@ template <int KIND>
 __device__ __forceinline__ uint32_t bucket_of(uint32_t u, const BucketParams &p) {
   if constexpr (KIND == kRadix) {
     return (u >> p.shift) & p.mask;
+  } else if constexpr (KIND == kDeltaShift) {
+    const uint32_t q = u >> p.shift;
+    return q < p.m1 ? q : p.m1;
   } else if constexpr (KIND == kIdentity) {
     return u < p.m1 ? u : p.m1;
   } else {
@@ -88,6 +101,10 @@ __device__ __forceinline__ uint32_t peer_mask_ballot(uint32_t b, uint32_t active
 // ---------------------------------------------------------------- PTX: smem address
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- PTX: mbarrier + TMA bulk copy

@@ -2,5 +2,5 @@
 #include "ms_dispatch.cuh"
 
 namespace ms {
-MS_INSTANTIATE_KIND(kDelta)
+template struct Launch<kDelta>;
 }  // namespace ms

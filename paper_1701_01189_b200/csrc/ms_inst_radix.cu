@@ -2,5 +2,5 @@
 #include "ms_dispatch.cuh"
 
 namespace ms {
-MS_INSTANTIATE_KIND(kRadix)
+template struct Launch<kRadix>;
 }  // namespace ms

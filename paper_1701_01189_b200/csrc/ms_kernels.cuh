@@ -1,128 +1,97 @@
-// ms_kernels.cuh -- the three stages of the multisplit on sm_100a.
+// ms_kernels.cuh -- the multisplit on sm_100a as the paper's lambda-level
+// localization (Sec.4.4, Eq.3) mapped onto B200:
 //
-//   KH  prescan  : per-tile bucket histogram H[l][j]          (Alg.1)
-//   KG  scan     : decoupled-lookback exclusive scan of the
-//                  row-vectorized H -> G, bucket bases        (Alg.1)
-//   KS  postscan : tile-local stable rank + reorder in smem,
-//                  coalesced scatter                          (Eq.4, Sec.5.6.2)
+//   level 0: G CTA ranges of K consecutive tiles      -> H = [h_{j,l0}] is m x G
+//   level 1: tiles of T elements inside a range        -> running per-bucket offsets
+//   level 2: warps inside a tile, level 3: 32-wide windows inside a warp (Eq.4)
 //
-// Layout in HBM: H/G tile-major (H[l*m + j]) so that every tile writes and
-// reads m contiguous words.  G holds only the column part sum_{l'<l} h_{j,l'}
-// of Eq.(2); the bucket bases sum_{j'<j} sum_l h_{j',l} live in a separate
-// (m+1)-word array written by the last scan CTA, and the postscan adds them.
+//   KU  prescan:   range histogram R[c][j] = h_{j,c} (level-0 column of H)
+//   KF  scan + postscan: each CTA scans the small m x G matrix R
+//       (Eq.3 terms 1-2), then for every tile of its range, in order: stable
+//       tile-local rank (Eq.4), tile-local reorder in shared memory
+//       (Sec.5.6.2), coalesced scatter of each bucket run.
+//
+// Also here: KH, the tile-granular prescan H[l][j] of Eq.(2) used by the
+// stage API and by the paper-faithful three-launch mode (KH -> KG -> KF).
+//
+// Citations "P:nnn" are lines of the paper's LaTeX source.
 #pragma once
 #include "ms_device.cuh"
 
 namespace ms {
 
-// Histogram / rank strategies (picked per m by the host dispatcher).
-enum Strategy : int {
-  kCount1 = 0,  // m <= 2: per-thread count of bucket 1 (KH) / one ballot per window (KS)
-  kPeers = 1,   // ceil(log2 m) ballots -> peer mask, leader update (Alg.2/3)
-  kMatch = 2,   // __match_any_sync peer mask, leader update
-  kAtomic = 3,  // KH only: one shared-memory atomic per key into warp-private counters
-};
-
-// Status word of the decoupled look-back: high 32 bits = flag, low = value.
-constexpr unsigned long long kFlagAggregate = 1ull << 32;
-constexpr unsigned long long kFlagInclusive = 2ull << 32;
-
 // ============================================================================
-// KH: prescan.  One CTA per tile of kTile keys.  Keys are read with 128-bit
-// streaming loads (order is irrelevant for a histogram).  Per-warp counters
-// live in shared memory (warp-level privatization); the tile
-// column of H is their sum.  CTA b also zeroes slice b of the look-back
-// status array (and CTA 0 the ticket / error words) for the following KG.
+// Shared histogram helpers.  m <= 2 counts ones in registers; otherwise each
+// warp owns a private row of m counters in shared memory (warp-level
+// privatization) updated with shared-memory atomics (measured
+// cheapest on B200, profiles/r01/v0_summary.md).
 // ============================================================================
-template <int KIND, int STRAT, int LOGM>
-__global__ void __launch_bounds__(kThreads, 2)
-    kh_prescan(const uint32_t *__restrict__ keys, uint32_t n, BucketParams bp,
-               uint32_t *__restrict__ H, unsigned long long *__restrict__ zero_status,
-               uint32_t zero_words, uint32_t *__restrict__ hdr) {
-  extern __shared__ uint32_t kh_smem[];  // [kWarps][m]
-  const uint32_t m = bp.m;
+template <int KIND, bool SMALLM>
+__device__ __forceinline__ void hist_add(uint32_t key, const BucketParams &bp, uint32_t *row,
+                                         uint32_t &ones) {
+  const uint32_t b = bucket_of<KIND>(key, bp);
+  if constexpr (SMALLM) {
+    ones += b;
+  } else {
+    atomicAdd(row + b, 1u);
+  }
+}
+
+// Count keys[lo, hi) into the CTA's counters (vector loads when aligned).
+template <int KIND, bool SMALLM>
+__device__ __forceinline__ void hist_range(const uint32_t *__restrict__ keys, uint32_t lo,
+                                           uint32_t hi, const BucketParams &bp, uint32_t *row,
+                                           uint32_t &ones) {
+  const uint32_t tid = threadIdx.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys + lo) & 15u) == 0);
+  uint32_t i = lo;
+  if (aligned) {
+    const uint4 *v = reinterpret_cast<const uint4 *>(keys + lo);
+    const uint32_t nv = (hi - lo) >> 2;
+    uint32_t j = tid;
+    for (; j + 3u * kThreads < nv; j += 4u * kThreads) {  // 4 x 16 B in flight per thread
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = ldg_stream_v4(v + j + (uint32_t)u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        hist_add<KIND, SMALLM>(q[u].x, bp, row, ones);
+        hist_add<KIND, SMALLM>(q[u].y, bp, row, ones);
+        hist_add<KIND, SMALLM>(q[u].z, bp, row, ones);
+        hist_add<KIND, SMALLM>(q[u].w, bp, row, ones);
+      }
+    }
+    for (; j < nv; j += kThreads) {
+      const uint4 q = ldg_stream_v4(v + j);
+      hist_add<KIND, SMALLM>(q.x, bp, row, ones);
+      hist_add<KIND, SMALLM>(q.y, bp, row, ones);
+      hist_add<KIND, SMALLM>(q.z, bp, row, ones);
+      hist_add<KIND, SMALLM>(q.w, bp, row, ones);
+    }
+    i = lo + (nv << 2);
+  }
+  for (i += tid; i < hi; i += kThreads) hist_add<KIND, SMALLM>(__ldg(keys + i), bp, row, ones);
+}
+
+// Sum the CTA's counters and write m words to out[0..m).  `total` = elements counted.
+template <bool SMALLM>
+__device__ __forceinline__ void hist_flush(uint32_t *cnt, uint32_t m, uint32_t ones,
+                                           uint32_t total, uint32_t *__restrict__ out,
+                                           uint32_t *s_red) {
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t tile = blockIdx.x;
-  const uint32_t tile_start = tile * (uint32_t)kTile;
-  const uint32_t tile_n = min((uint32_t)kTile, n - tile_start);
-
-  // zero this CTA's slice of the look-back status array (consumed by KG)
-  if (zero_status) {
-    const uint32_t per = (zero_words + gridDim.x - 1) / gridDim.x;
-    const uint32_t lo = tile * per, hi = min(zero_words, lo + per);
-    for (uint32_t i = lo + tid; i < hi; i += kThreads) zero_status[i] = 0ull;
-    if (tile == 0 && tid < 2) hdr[tid] = 0u;  // [0] error flag, [1] scan ticket
-  }
-
-  uint32_t *cnt = kh_smem + warp * m;
-  if constexpr (STRAT != kCount1) {
-    for (uint32_t i = tid; i < kWarps * m; i += kThreads) kh_smem[i] = 0u;
-    __syncthreads();
-  }
-
-  // each warp owns a contiguous quarter... of the tile: 4 x 128-bit loads / lane
-  constexpr int kVec = kItems / 4;
-  const uint32_t wbase = warp * (kItems * 32);
-  uint32_t ones = 0, valid_cnt = 0;
-  const bool full = (tile_n == (uint32_t)kTile);
-  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0);
-
+  if constexpr (SMALLM) {
 #pragma unroll
-  for (int v = 0; v < kVec; ++v) {
-    const uint32_t e0 = wbase + (uint32_t)v * 128u + lane * 4u;  // first element of this lane
-    uint32_t k4[4];
-    bool ok4[4];
-    if (full && aligned) {
-      uint4 q = ldg_stream_v4(reinterpret_cast<const uint4 *>(keys + tile_start + e0));
-      k4[0] = q.x; k4[1] = q.y; k4[2] = q.z; k4[3] = q.w;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) ok4[c] = true;
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        ok4[c] = (e0 + c) < tile_n;
-        k4[c] = ok4[c] ? __ldg(keys + tile_start + e0 + c) : 0u;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint32_t b = bucket_of<KIND>(k4[c], bp);
-      if constexpr (STRAT == kCount1) {
-        ones += ok4[c] ? b : 0u;
-        valid_cnt += ok4[c] ? 1u : 0u;
-      } else if constexpr (STRAT == kAtomic) {
-        if (ok4[c]) atomicAdd(cnt + b, 1u);
-      } else {
-        const uint32_t active = __ballot_sync(0xFFFFFFFFu, ok4[c]);
-        uint32_t peers;
-        if constexpr (STRAT == kMatch) {
-          peers = __match_any_sync(0xFFFFFFFFu, ok4[c] ? b : 0xFFFFFFFFu) & active;
-        } else {
-          peers = peer_mask_ballot<LOGM>(b, active, ok4[c]);
-        }
-        const bool leader = ok4[c] && ((peers & lanemask_lt()) == 0u);
-        if (leader) atomicAdd(cnt + b, (uint32_t)__popc(peers));
-      }
-    }
-  }
-
-  if constexpr (STRAT == kCount1) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ones += __shfl_xor_sync(0xFFFFFFFFu, ones, o);
-      valid_cnt += __shfl_xor_sync(0xFFFFFFFFu, valid_cnt, o);
-    }
-    __shared__ uint32_t w1[kWarps], wv[kWarps];
-    if (lane == 0) { w1[warp] = ones; wv[warp] = valid_cnt; }
+    for (int o = 16; o > 0; o >>= 1) ones += __shfl_xor_sync(0xFFFFFFFFu, ones, o);
+    if (lane == 0) s_red[warp] = ones;
     __syncthreads();
     if (tid == 0) {
-      uint32_t o = 0, v = 0;
-      for (int w = 0; w < kWarps; ++w) { o += w1[w]; v += wv[w]; }
+      uint32_t o = 0;
+      for (int w = 0; w < kWarps; ++w) o += s_red[w];
       if (m == 1) {
-        H[tile] = v;
+        out[0] = total;
       } else {
-        H[tile * 2 + 0] = v - o;
-        H[tile * 2 + 1] = o;
+        out[0] = total - o;
+        out[1] = o;
       }
     }
   } else {
@@ -130,140 +99,172 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (uint32_t j = tid; j < m; j += kThreads) {
       uint32_t s = 0;
 #pragma unroll 4
-      for (int w = 0; w < kWarps; ++w) s += kh_smem[w * m + j];
-      H[tile * m + j] = s;
+      for (int w = 0; w < kWarps; ++w) s += cnt[w * m + j];
+      out[j] = s;
     }
   }
 }
 
 // ============================================================================
-// KS: postscan.  One CTA per tile.
-//  1. TMA bulk copy of the tile's keys (and values) into shared memory.
-//  2. Each warp ranks its contiguous kItems*32 elements window by window
-//     (lane i holds element i of the window): rank = warp-private
-//     running count of the bucket + same-bucket lanes below (Eq.4 terms 1-2).
-//  3. Block exclusive scan of the warp counts in (bucket, warp) order gives
-//     the tile's stable local multisplit slot (Eq.4 term 3 + tile bucket base,
-//     block-level reordering Sec.5.6.2).
-//  4. Keys (then values) are written to their slots in shared memory.
-//  5. Slot s of bucket b goes to out[G[l][b] + base[b] + s - tilebase[b]]:
-//     consecutive threads write consecutive addresses inside each bucket run.
-// SINGLE (n <= kTile): G = 0 and base = tile bases; writes bucket_offsets.
+// KU: range histogram (level-0 prescan).  CTA c counts keys
+// [c*E, min(n, (c+1)*E)) where E = K tiles, and writes R[c][0..m).
 // ============================================================================
-struct KsArgs {
+template <int KIND, bool SMALLM>
+__global__ void __launch_bounds__(kThreads)
+    ku_range_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t elems_per_cta,
+                  BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  extern __shared__ uint32_t ku_smem[];  // [kWarps][m]
+  __shared__ uint32_t s_red[kWarps];
+  const uint32_t m = bp.m, tid = threadIdx.x;
+  const uint32_t lo = blockIdx.x * elems_per_cta;
+  const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + elems_per_cta);
+  if (hdr && blockIdx.x == 0 && tid == 0) hdr[0] = 0u;  // error flag of this call (set by KF)
+  if constexpr (!SMALLM) {
+    for (uint32_t i = tid; i < kWarps * m; i += kThreads) ku_smem[i] = 0u;
+    __syncthreads();
+  }
+  uint32_t ones = 0;
+  hist_range<KIND, SMALLM>(keys, lo, hi, bp, ku_smem + (tid >> 5) * m, ones);
+  hist_flush<SMALLM>(ku_smem, m, ones, hi - lo, R + (size_t)blockIdx.x * m, s_red);
+}
+
+// ============================================================================
+// KH: tile-granular prescan (stage API and three-launch mode).  CTA l counts
+// tile [l*T, min(n, (l+1)*T)) into H[l][0..m)  (Eq.2's h_{j,l}, Alg.1).
+// ============================================================================
+template <int KIND, bool SMALLM>
+__global__ void __launch_bounds__(kThreads)
+    kh_tile_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t tile, BucketParams bp,
+                 uint32_t *__restrict__ H, uint32_t *__restrict__ hdr) {
+  extern __shared__ uint32_t kh_smem[];
+  __shared__ uint32_t s_red[kWarps];
+  const uint32_t m = bp.m, tid = threadIdx.x;
+  const uint32_t lo = blockIdx.x * tile;
+  const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + tile);
+  if (hdr && blockIdx.x == 0 && tid == 0) hdr[0] = 0u;
+  if constexpr (!SMALLM) {
+    for (uint32_t i = tid; i < kWarps * m; i += kThreads) kh_smem[i] = 0u;
+    __syncthreads();
+  }
+  uint32_t ones = 0;
+  hist_range<KIND, SMALLM>(keys, lo, hi, bp, kh_smem + (tid >> 5) * m, ones);
+  hist_flush<SMALLM>(kh_smem, m, ones, hi - lo, H + (size_t)blockIdx.x * m, s_red);
+}
+
+// ============================================================================
+// KF: scan + postscan.
+// ============================================================================
+enum KfMode : int {
+  kModeRange = 0,   // offsets from the range histograms R (two launches: KU, KF)
+  kModeTileG = 1,   // offsets G[l][j] given per tile (three launches: KH, KG, KF)
+  kModeSingle = 2,  // n <= T: one tile, one launch; the tile histogram is global
+};
+
+struct KfArgs {
   const uint32_t *keys_in;
   const uint32_t *vals_in;
   uint32_t *keys_out;
   uint32_t *vals_out;
   uint32_t n;
-  const uint32_t *G;     // [L][m] column prefix (multi-tile)
-  const uint32_t *base;  // [m+1] bucket bases (multi-tile)
-  uint32_t *hdr;         // [0] error flag
+  uint32_t num_tiles;
+  uint32_t tiles_per_cta;
+  uint32_t num_ranges;
+  const uint32_t *R;   // [num_ranges][m]     (kModeRange)
+  const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
+  const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
+  uint32_t *hdr;       // [0] key-domain error flag
   uint32_t *bucket_offsets;
-  int single;
+  int mode;
   int use_tma;
 };
 
-__host__ __device__ constexpr uint32_t ks_cnt_stride(uint32_t m) { return m + 1; }
-
-__host__ __device__ inline size_t ks_smem_bytes(uint32_t m, bool pairs) {
-  // keys tile (+ values tile) + counters [kWarps][m+1] + delta[m] + scratch
-  return (size_t)kTile * 4u * (pairs ? 2u : 1u) + (size_t)kWarps * ks_cnt_stride(m) * 4u +
-         (size_t)m * 4u + 64u * 4u;
+// Shared memory carve-up (bytes): 2 stages x (keys [+ values]) | bucket byte per
+// reordered slot | per-warp peer masks [W][m] | per-warp counts [W][m] | delta[m]
+__host__ __device__ constexpr size_t kf_stage_words(bool pairs) {
+  return (size_t)(pairs ? kTilePairs : kTileKeys) * (pairs ? 2u : 1u);
+}
+__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
+  const size_t T = pairs ? kTilePairs : kTileKeys;
+  const size_t mm = m < 2 ? 2 : m;
+  return 2 * kf_stage_words(pairs) * 4 + T + 2 * (size_t)kWarps * mm * 4 + mm * 4;
 }
 
-template <int KIND, bool PAIRS, int STRAT, int LOGM>
-__global__ void __launch_bounds__(kThreads, 2) ks_postscan(KsArgs a, BucketParams bp) {
-  extern __shared__ __align__(128) uint32_t ks_smem[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t s_wsum[kWarps];
+template <int KIND, bool PAIRS, bool SMALLM, bool FULL>
+__device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
+                                        uint32_t tn, uint32_t *s_keys, uint32_t *s_vals,
+                                        uint8_t *s_bkt, uint32_t *s_mask, uint32_t *s_cnt,
+                                        uint32_t *s_delta, uint32_t *s_wsum, uint32_t &running) {
+  constexpr int ITEMS = TileCfg<PAIRS>::kItems;
+  constexpr uint32_t RE_SMALL = 2;
   const uint32_t m = bp.m;
-  uint32_t *s_keys = ks_smem;
-  uint32_t *s_vals = ks_smem + kTile;
-  uint32_t *s_cnt = ks_smem + kTile * (PAIRS ? 2 : 1);  // [kWarps][m+1], warp-major
-  uint32_t *s_delta = s_cnt + kWarps * ks_cnt_stride(m);
-  const uint32_t stride = ks_cnt_stride(m);
-
+  const uint32_t re = SMALLM ? RE_SMALL : m;  // counters per warp row
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t tile = blockIdx.x;
-  const uint32_t tile_start = tile * (uint32_t)kTile;
-  const uint32_t tile_n = min((uint32_t)kTile, a.n - tile_start);
+  const uint32_t lt = lanemask_lt(), lanebit = 1u << lane;
+  const uint32_t wbase = warp * (ITEMS * 32);
+  uint32_t *mrow = s_mask + warp * re;
+  uint32_t *crow = s_cnt + warp * re;
 
-  // ---- 1. load the tile into shared memory -------------------------------
-  const uint32_t bulk_elems = a.use_tma ? (tile_n & ~3u) : 0u;  // 16-byte multiple
-  if (tid == 0 && a.use_tma) mbar_init(&bar, 1);
-  for (uint32_t i = bulk_elems + tid; i < tile_n; i += kThreads) {  // ragged tail / no-TMA
-    s_keys[i] = __ldg(a.keys_in + tile_start + i);
-    if constexpr (PAIRS) s_vals[i] = __ldg(a.vals_in + tile_start + i);
-  }
-  for (uint32_t i = tid; i < kWarps * stride; i += kThreads) s_cnt[i] = 0u;
-  if (a.single && tid == 0) a.hdr[0] = 0u;
-  __syncthreads();
-  if (a.use_tma) {
-    if (tid == 0 && bulk_elems > 0) {
-      const uint64_t pol = policy_evict_first();
-      mbar_arrive_expect_tx(&bar, bulk_elems * 4u * (PAIRS ? 2u : 1u));
-      tma_load_1d(s_keys, a.keys_in + tile_start, bulk_elems * 4u, &bar, pol);
-      if constexpr (PAIRS) tma_load_1d(s_vals, a.vals_in + tile_start, bulk_elems * 4u, &bar, pol);
+  // ---- 1. warp-level stable ranking, window by window (Eq.4 terms 1-2) ----
+  if constexpr (!SMALLM) {
+    for (uint32_t j = lane; j < m; j += 32) {
+      mrow[j] = 0u;
+      crow[j] = 0u;
     }
-    if (bulk_elems > 0) mbar_wait(&bar, 0);
+    __syncwarp();
   }
-
-  // ---- 2. warp-level ranking ---------------------------------------------
-  const uint32_t wbase = warp * (kItems * 32);
-  uint32_t key[kItems];
-  uint32_t packed[kItems];  // (bucket << 16) | rank within warp
-  const uint32_t lt = lanemask_lt();
-  bool dom_err = false;
-  uint32_t c0 = 0, c1 = 0;  // kCount1 running counts (warp-uniform)
+  uint32_t pk[ITEMS];  // (bucket << 16) | rank within the warp
+  uint32_t c0 = 0, c1 = 0;
+  bool derr = false;
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-    const bool valid = idx < tile_n;
-    key[i] = valid ? s_keys[idx] : 0u;
-    const uint32_t b = bucket_of<KIND>(key[i], bp);
-    dom_err |= valid && key_domain_error<KIND>(key[i], bp);
-    if (wbase + (uint32_t)i * 32u >= tile_n) {  // window entirely past the tail
-      packed[i] = 0u;
-      continue;
-    }
-    if constexpr (STRAT == kCount1) {
-      const uint32_t vmask = __ballot_sync(0xFFFFFFFFu, valid);
-      const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b == 1u);
-      const uint32_t zeros = vmask & ~ones;
-      const uint32_t r = b ? c1 + __popc(ones & lt) : c0 + __popc(zeros & lt);
-      packed[i] = (b << 16) | r;
+    const bool valid = FULL || idx < tn;
+    const uint32_t key = valid ? s_keys[idx] : 0u;
+    const uint32_t b = bucket_of<KIND>(key, bp);
+    if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key, bp);
+    pk[i] = 0u;
+    if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: window past the tail
+    uint32_t r;
+    if constexpr (SMALLM) {
+      // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
+      const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
+      const uint32_t vm = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
+      const uint32_t zeros = vm & ~ones;
+      r = b ? c1 + __popc(ones & lt) : c0 + __popc(zeros & lt);
       c1 += __popc(ones);
       c0 += __popc(zeros);
     } else {
-      const uint32_t active = __ballot_sync(0xFFFFFFFFu, valid);
-      uint32_t peers;
-      if constexpr (STRAT == kMatch) {
-        peers = __match_any_sync(0xFFFFFFFFu, valid ? b : 0xFFFFFFFFu) & active;
-      } else {
-        peers = peer_mask_ballot<LOGM>(b, active, valid);
-      }
+      // peer mask by shared-memory OR of lane bits (replaces the log2 m ballots of
+      // Alg.3 P:909-930 with one atomic), then rank = warp count + lanes below
+      if (valid) atomicOr(mrow + b, lanebit);
+      __syncwarp();
+      const uint32_t peers = valid ? mrow[b] : 0u;
+      const uint32_t cnt = valid ? crow[b] : 0u;
       const uint32_t below = peers & lt;
-      uint32_t *ctr = s_cnt + warp * stride + b;
-      const uint32_t old = valid ? *ctr : 0u;
+      r = cnt + __popc(below);
       __syncwarp();
-      if (valid && below == 0u) *ctr = old + (uint32_t)__popc(peers);
+      if (valid && below == 0u) {  // group leader: clear the mask, advance the count
+        mrow[b] = 0u;
+        crow[b] = cnt + __popc(peers);
+      }
       __syncwarp();
-      packed[i] = (b << 16) | (old + (uint32_t)__popc(below));
     }
+    pk[i] = (b << 16) | r;
   }
-  if constexpr (STRAT == kCount1) {
+  if constexpr (SMALLM) {
     if (lane == 0) {
-      s_cnt[warp * stride + 0] = c0;
-      if (m > 1) s_cnt[warp * stride + 1] = c1;
+      crow[0] = c0;
+      crow[1] = c1;
     }
   }
   if constexpr (KIND == kIdentity) {
-    if (__any_sync(0xFFFFFFFFu, dom_err) && lane == 0) atomicOr(a.hdr, 1u);
+    if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
   }
   __syncthreads();
 
-  // ---- 3. block exclusive scan of counts in (bucket, warp) order ---------
+  // ---- 2. tile exclusive scan of the counts in (bucket, warp) order ----------
+  // (Eq.4 term 3 plus the tile's bucket bases: a stable local multisplit of
+  // the tile, Sec.4.7 / Sec.5.6.2)
   {
     const uint32_t total = m * kWarps;
     const uint32_t per = (total + kThreads - 1) / kThreads;  // <= 8
@@ -272,12 +273,9 @@ __global__ void __launch_bounds__(kThreads, 2) ks_postscan(KsArgs a, BucketParam
     uint32_t s = 0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const uint32_t q = q0 + e;
-      v[e] = 0;
-      if (e < (int)per && q < total) {
-        const uint32_t b = q / kWarps, w = q % kWarps;
-        v[e] = s_cnt[w * stride + b];
-      }
+      const uint32_t q = q0 + (uint32_t)e;
+      v[e] = 0u;
+      if ((uint32_t)e < per && q < total) v[e] = s_cnt[(q % kWarps) * re + q / kWarps];
       s += v[e];
     }
     uint32_t incl = s;
@@ -289,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2) ks_postscan(KsArgs a, BucketParam
     if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
+      const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
       uint32_t xi = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -302,62 +300,196 @@ __global__ void __launch_bounds__(kThreads, 2) ks_postscan(KsArgs a, BucketParam
     uint32_t run = s_wsum[warp] + incl - s;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const uint32_t q = q0 + e;
-      if (e < (int)per && q < total) {
-        const uint32_t b = q / kWarps, w = q % kWarps;
-        s_cnt[w * stride + b] = run;
+      const uint32_t q = q0 + (uint32_t)e;
+      if ((uint32_t)e < per && q < total) {
+        s_cnt[(q % kWarps) * re + q / kWarps] = run;
         run += v[e];
       }
     }
   }
   __syncthreads();
-  // tile bucket base = scanned (b, warp 0); delta[b] = global start - tile base
-  for (uint32_t b = tid; b < m; b += kThreads) {
-    const uint32_t tb = s_cnt[b];  // warp 0 row
-    if (a.single) {
-      s_delta[b] = 0u;
-      if (a.bucket_offsets) a.bucket_offsets[b] = tb;
-    } else {
-      s_delta[b] = a.G[(size_t)tile * m + b] + a.base[b] - tb;
-    }
-  }
-  if (a.single && tid == 0 && a.bucket_offsets) a.bucket_offsets[m] = tile_n;
 
-  // ---- 4. reorder into shared memory --------------------------------------
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-    if (idx < tile_n) {
-      const uint32_t b = packed[i] >> 16;
-      const uint32_t slot = s_cnt[warp * stride + b] + (packed[i] & 0xFFFFu);
-      packed[i] = slot;
-      s_keys[slot] = key[i];
+  // ---- 3. per bucket: global start of this tile's run (Eq.2/3 terms 1-2) -----
+  if (tid < m) {
+    const uint32_t tb = s_cnt[tid];  // warp 0 row = tile bucket base
+    const uint32_t te = tid + 1 < m ? s_cnt[tid + 1] : tn;
+    uint32_t d;
+    if (a.mode == kModeSingle) {
+      d = 0u;
+      if (a.bucket_offsets) {
+        a.bucket_offsets[tid] = tb;
+        if (tid == m - 1) a.bucket_offsets[m] = tn;
+      }
+    } else if (a.mode == kModeTileG) {
+      d = a.Gt[(size_t)tile * m + tid] + a.base[tid] - tb;
+    } else {
+      d = running - tb;
+      running += te - tb;
     }
+    s_delta[tid] = d;
   }
-  if constexpr (PAIRS) {
-    uint32_t val[kItems];
+
+  // ---- 4. reorder the tile in shared memory (stable local multisplit) --------
+  // keys (and values) are re-read in input order into registers only now, so
+  // that the ranking phase holds just the packed ranks
+  uint32_t key[ITEMS];
+  uint32_t val[PAIRS ? ITEMS : 1];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-      val[i] = idx < tile_n ? s_vals[idx] : 0u;
-    }
-    __syncthreads();
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
+    key[i] = (FULL || idx < tn) ? s_keys[idx] : 0u;
+    if constexpr (PAIRS) val[i] = (FULL || idx < tn) ? s_vals[idx] : 0u;
+    pk[i] = crow[pk[i] >> 16] + (pk[i] & 0xFFFFu) + (pk[i] & 0xFF0000u) * 256u;  // slot | b << 24
+  }
+  __syncthreads();  // every input-order element is in registers before slots are overwritten
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-      if (idx < tile_n) s_vals[packed[i]] = val[i];
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
+    if (FULL || idx < tn) {
+      const uint32_t slot = pk[i] & 0xFFFFFFu;
+      s_keys[slot] = key[i];
+      s_bkt[slot] = (uint8_t)(pk[i] >> 24);
+      if constexpr (PAIRS) s_vals[slot] = val[i];
     }
   }
   __syncthreads();
 
-  // ---- 5. coalesced scatter of bucket runs --------------------------------
-#pragma unroll 4
-  for (uint32_t s = tid; s < tile_n; s += kThreads) {
-    const uint32_t k = s_keys[s];
-    const uint32_t b = bucket_of<KIND>(k, bp);
-    const uint32_t p = s_delta[b] + s;
-    a.keys_out[p] = k;
-    if constexpr (PAIRS) a.vals_out[p] = s_vals[s];
+  // ---- 5. coalesced scatter: slot s of bucket b -> delta[b] + s --------------
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t s = (uint32_t)i * kThreads + tid;
+    if (FULL || s < tn) {
+      const uint32_t p = s_delta[s_bkt[s]] + s;
+      a.keys_out[p] = s_keys[s];
+      if constexpr (PAIRS) a.vals_out[p] = s_vals[s];
+    }
+  }
+  __syncthreads();
+}
+
+template <int KIND, bool PAIRS, bool SMALLM>
+__global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams bp) {
+  constexpr uint32_t T = TileCfg<PAIRS>::kTile;
+  constexpr uint32_t SW = (uint32_t)kf_stage_words(PAIRS);
+  extern __shared__ __align__(128) uint8_t kf_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ uint32_t s_wsum[kWarps];
+  const uint32_t m = bp.m;
+  const uint32_t mm = m < 2 ? 2 : m;
+  uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
+  uint8_t *s_bkt = kf_smem + 2 * SW * 4;
+  uint32_t *s_mask = reinterpret_cast<uint32_t *>(s_bkt + T);
+  uint32_t *s_cnt = s_mask + kWarps * mm;
+  uint32_t *s_delta = s_cnt + kWarps * mm;
+  const uint32_t tid = threadIdx.x;
+
+  uint32_t t0 = 0, t1 = 1;
+  if (a.mode != kModeSingle) {
+    t0 = blockIdx.x * a.tiles_per_cta;
+    t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
+    if (t0 >= t1) return;
+  }
+  auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
+  auto issue = [&](uint32_t t, int st) {  // one elected thread starts the TMA bulk copy
+    if (tid == 0 && t < t1 && a.use_tma && tile_n(t) == T) {
+      uint32_t *dst = stage0 + st * SW;
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
+      tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
+      if constexpr (PAIRS) tma_load_1d(dst + T, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    if (a.mode == kModeSingle) a.hdr[0] = 0u;
+  }
+  __syncthreads();
+  issue(t0, 0);
+  issue(t0 + 1, 1);
+
+  // ---- level-0 scan (Eq.3 terms 1-2 over the m x G matrix R) -------------------
+  // thread b < m ends with running = sum_{j<b} total_j + sum_{c<blockIdx} R[c][b]
+  uint32_t running = 0;
+  if (a.mode == kModeRange) {
+    uint32_t *s_tot = reinterpret_cast<uint32_t *>(s_bkt);  // scratch before the first tile
+    uint32_t *s_pre = s_tot + kThreads;
+    const uint32_t P = kThreads / m;  // row groups (>= 2)
+    const uint32_t b = tid % m, p = tid / m;
+    uint32_t tot = 0, pre = 0;
+    if (p < P) {
+      for (uint32_t r = p; r < a.num_ranges; r += P) {
+        const uint32_t v = a.R[(size_t)r * m + b];
+        tot += v;
+        pre += r < blockIdx.x ? v : 0u;
+      }
+      s_tot[p * m + b] = tot;
+      s_pre[p * m + b] = pre;
+    }
+    __syncthreads();
+    uint32_t t = 0, pr = 0;
+    if (tid < m) {
+      for (uint32_t q = 0; q < P; ++q) {
+        t += s_tot[q * m + tid];
+        pr += s_pre[q * m + tid];
+      }
+    }
+    // exclusive scan of the bucket totals across threads 0..m-1 (block scan)
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += x;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
+      uint32_t xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+        if (lane >= (uint32_t)o) xi += y;
+      }
+      if (lane < (uint32_t)kWarps) s_wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    if (tid < m) {
+      const uint32_t gbase = s_wsum[warp] + incl - t;
+      running = gbase + pr;
+      if (blockIdx.x == 0 && a.bucket_offsets) {
+        a.bucket_offsets[tid] = gbase;
+        if (tid == m - 1) a.bucket_offsets[m] = gbase + t;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- tiles of this range, in order, double-buffered TMA ----------------------
+  uint32_t k = 0;
+  for (uint32_t t = t0; t < t1; ++t, ++k) {
+    const int st = (int)(k & 1u);
+    uint32_t *s_keys = stage0 + st * SW;
+    uint32_t *s_vals = s_keys + T;
+    const uint32_t tn = tile_n(t);
+    if (a.use_tma && tn == T) {
+      mbar_wait(&bar[st], (k >> 1) & 1u);
+    } else {  // ragged last tile / unaligned input: plain loads
+      for (uint32_t i = tid; i < tn; i += kThreads) {
+        s_keys[i] = __ldg(a.keys_in + (size_t)t * T + i);
+        if constexpr (PAIRS) s_vals[i] = __ldg(a.vals_in + (size_t)t * T + i);
+      }
+      __syncthreads();
+    }
+    if (tn == T)
+      kf_tile<KIND, PAIRS, SMALLM, true>(a, bp, t, tn, s_keys, s_vals, s_bkt, s_mask, s_cnt,
+                                         s_delta, s_wsum, running);
+    else
+      kf_tile<KIND, PAIRS, SMALLM, false>(a, bp, t, tn, s_keys, s_vals, s_bkt, s_mask, s_cnt,
+                                          s_delta, s_wsum, running);
+    if (tid == 0) fence_proxy_async_smem();  // generic-proxy smem writes before the next TMA
+    issue(t + 2, st);
   }
 }
 

@@ -5,6 +5,10 @@
 
 namespace ms {
 
+// Status word of the decoupled look-back: high 32 bits = flag, low = value.
+constexpr unsigned long long kFlagAggregate = 1ull << 32;
+constexpr unsigned long long kFlagInclusive = 2ull << 32;
+
 // ============================================================================
 // KG: decoupled look-back scan over the tile-major H.  CTA (ticket c) owns
 // tiles [c*C, (c+1)*C) x all m buckets.  Threads are (group g, bucket j)

@@ -96,7 +96,7 @@ def test_host_argument_errors_return_before_launch(lib):
                                    None) == _lib.MS_ERR_INVALID_VALUE
     assert lib.ms_radix_sort_keys(fake, other, 10, 0, 32, 9, ws, 1 << 30, None) == _lib.MS_ERR_INVALID_VALUE
     assert lib.ms_radix_sort_keys(fake, other, 10, 0, 32, 8, ws, 10, None) == _lib.MS_ERR_WORKSPACE
-    assert lib.ms_stage_prescan(fake, 10, ctypes.byref(fn), other, 1234, None) == _lib.MS_ERR_INVALID_VALUE
+    assert lib.ms_stage_prescan(fake, 10, ctypes.byref(fn), other, 0, None) == _lib.MS_ERR_INVALID_VALUE
 
 
 def test_workspace_sizes(lib):

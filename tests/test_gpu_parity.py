@@ -74,11 +74,11 @@ def test_spec_grid_identity_radix(kind, m, n):
     check_multisplit(keys, gen.values(n, seed=2), ob, pb)
 
 
-T = 8192  # ms.tile_size(); checked below
+T = 8192  # ms.tile_size() for keys (4096 for pairs); checked below
 
 
 def test_tile_size():
-    assert ms.tile_size() == T
+    assert ms.tile_size(256, False) == T and ms.tile_size(256, True) == T // 2
 
 
 @pytest.mark.parametrize("n", [T - 1, T, T + 1, 2 * T - 3, 3 * T + 5, 37 * T + 4097])
@@ -142,8 +142,9 @@ def test_identity_domain_error_flag(n):
 def test_stage_prescan(m, n):
     ob, pb, gk = bucket_pair("delta", m)
     keys = gen.keys(n, seed=7, dist=gen.DIST_BINOMIAL, **gk)
-    H = ms.prescan(dev(keys), pb)
-    assert np.array_equal(host(H), oracle.tile_histogram(keys, ob, T))
+    for tile in (T, T // 2, 1000, 37):
+        H = ms.prescan(dev(keys), pb, tile=tile)
+        assert np.array_equal(host(H), oracle.tile_histogram(keys, ob, tile))
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (1, 256), (4096, 2), (4096, 32), (2049, 33), (32768, 256), (5, 255)])
@@ -182,6 +183,17 @@ def test_radix_sort_bits(args):
     ek, ev = oracle.radix_sort(keys, vals, b0, b1)
     ko, vo = ms.radix_sort(dev(keys), dev(vals), begin_bit=b0, end_bit=b1, bits_per_pass=r)
     assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+@pytest.mark.parametrize("m", [2, 37, 256])
+def test_three_launch_mode(monkeypatch, pairs, m):
+    # MS_PIPELINE=3pass: the paper's {tile histograms H, scan of H, postscan}
+    monkeypatch.setenv("MS_PIPELINE", "3pass")
+    ob, pb, gk = bucket_pair("delta", m)
+    n = 29 * T + 333
+    keys = gen.keys(n, seed=m, dist=gen.DIST_SKEW, **gk)
+    check_multisplit(keys, gen.values(n, seed=2) if pairs else None, ob, pb)
 
 
 def test_determinism_repeated_runs():
