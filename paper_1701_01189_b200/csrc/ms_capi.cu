@@ -38,7 +38,8 @@ uint32_t scan_chunk_tiles(uint32_t m) {
   return c < 1 ? 1 : c;
 }
 
-uint32_t tile_elems(bool pairs) { return pairs ? (uint32_t)kTilePairs : (uint32_t)kTileKeys; }
+uint32_t tile_elems(uint32_t m, bool pairs) { return kf_tile(pairs, m > 64); }
+uint32_t ctas_per_sm(uint32_t m, bool pairs) { return (uint32_t)kf_shape(pairs, m > 64).ctas_per_sm; }
 
 // Workspace: [hdr 256 B][base 1280 B][R or H: L*m words][KG status: nchunks*m u64]
 // (the level-0 histogram R needs G <= L rows; the three-launch mode needs L rows of H).
@@ -49,7 +50,7 @@ struct Layout {
 
 Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   Layout lo{};
-  lo.T = tile_elems(pairs);
+  lo.T = tile_elems(m, pairs);
   lo.base = kHdrBytes;
   lo.H = kHdrBytes + kBaseBytes;
   if (n <= lo.T) {  // single-CTA path: header only
@@ -245,7 +246,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
 
   // level-0 localization: G ranges of K consecutive tiles (2 CTAs per SM)
-  const uint32_t target = (uint32_t)sm_count() * 2u;
+  const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
   stage_event(0, s);
@@ -404,8 +405,7 @@ ms_status ms_device_status(const void *ws, void *stream) {
 }
 
 uint32_t ms_multisplit_tile_size(uint32_t m, int with_values) {
-  (void)m;
-  return tile_elems(with_values != 0);
+  return tile_elems(m, with_values != 0);
 }
 
 ms_status ms_stage_prescan(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn,

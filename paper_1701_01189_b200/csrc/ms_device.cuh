@@ -11,23 +11,11 @@ namespace ms {
 
 // ---------------------------------------------------------------- tunables
 constexpr int kWarp = 32;
-// One CTA = 16 warps.  A tile (the subproblem of the last localization level
-// reordered in shared memory) is 16 windows x 32 lanes per warp
-// for keys (8192 elements) and 8 windows per warp for pairs (4096): 32 KB of
-// keys either way.  B200's 227 KB of shared memory lets a tile be 8x the
-// paper's 1024-element BMS tile, so that at m = 256 the average
-// bucket run per key tile is 32 elements = 128 B of coalesced writes.
+// Histogram kernels use 16-warp CTAs; the postscan CTA shapes are in
+// ms_kernels.cuh (kf_shape).
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kMaxBuckets = 256;
-
-template <bool PAIRS>
-struct TileCfg {
-  static constexpr int kItems = PAIRS ? 8 : 16;  // windows per warp = elements per thread
-  static constexpr int kTile = kThreads * kItems;
-};
-constexpr int kTileKeys = TileCfg<false>::kTile;    // 8192
-constexpr int kTilePairs = TileCfg<true>::kTile;    // 4096
 
 // kDeltaShift is the internal form of DELTA when delta = 2^shift: floor(u/delta)
 // is a shift (the bench's equal-width buckets of P:1107 with m = 2^k).

@@ -43,27 +43,32 @@ cudaError_t Launch<KIND>::tile_hist(const uint32_t *keys, uint32_t n, uint32_t t
   return cudaGetLastError();
 }
 
-template <int KIND, bool PAIRS, bool SMALLM>
+template <int KIND, bool PAIRS, bool SMALLM, bool BIGM>
 static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
-  auto kern = kf_fused<KIND, PAIRS, SMALLM>;
+  constexpr KfShape sh = kf_shape(PAIRS, BIGM);
+  auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kf_smem_bytes(kMaxBuckets, PAIRS));
+                                         (int)kf_smem_bytes(BIGM ? kMaxBuckets : 64, PAIRS));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<grid, kThreads, kf_smem_bytes(bp.m, PAIRS), s>>>(a, bp);
+  kern<<<grid, sh.warps * 32, kf_smem_bytes(bp.m, PAIRS), s>>>(a, bp);
   return cudaGetLastError();
 }
 
 template <int KIND>
 cudaError_t Launch<KIND>::fused(bool pairs, const KfArgs &a, const BucketParams &bp,
                                 uint32_t grid, cudaStream_t s) {
-  const bool small = bp.m <= 2;
-  if (pairs)
-    return small ? kf_go<KIND, true, true>(a, bp, grid, s) : kf_go<KIND, true, false>(a, bp, grid, s);
-  return small ? kf_go<KIND, false, true>(a, bp, grid, s) : kf_go<KIND, false, false>(a, bp, grid, s);
+  if (bp.m <= 2)
+    return pairs ? kf_go<KIND, true, true, false>(a, bp, grid, s)
+                 : kf_go<KIND, false, true, false>(a, bp, grid, s);
+  if (bp.m <= 64)
+    return pairs ? kf_go<KIND, true, false, false>(a, bp, grid, s)
+                 : kf_go<KIND, false, false, false>(a, bp, grid, s);
+  return pairs ? kf_go<KIND, true, false, true>(a, bp, grid, s)
+               : kf_go<KIND, false, false, true>(a, bp, grid, s);
 }
 
 }  // namespace ms

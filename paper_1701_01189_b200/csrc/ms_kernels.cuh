@@ -49,12 +49,12 @@ __device__ __forceinline__ void hist_range(const uint32_t *__restrict__ keys, ui
     const uint4 *v = reinterpret_cast<const uint4 *>(keys + lo);
     const uint32_t nv = (hi - lo) >> 2;
     uint32_t j = tid;
-    for (; j + 3u * kThreads < nv; j += 4u * kThreads) {  // 4 x 16 B in flight per thread
-      uint4 q[4];
+    for (; j + 7u * kThreads < nv; j += 8u * kThreads) {  // 8 x 16 B in flight per thread
+      uint4 q[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = ldg_stream_v4(v + j + (uint32_t)u * kThreads);
+      for (int u = 0; u < 8; ++u) q[u] = ldg_stream_v4(v + j + (uint32_t)u * kThreads);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         hist_add<KIND, SMALLM>(q[u].x, bp, row, ones);
         hist_add<KIND, SMALLM>(q[u].y, bp, row, ones);
         hist_add<KIND, SMALLM>(q[u].z, bp, row, ones);
@@ -169,60 +169,85 @@ struct KfArgs {
   uint32_t num_tiles;
   uint32_t tiles_per_cta;
   uint32_t num_ranges;
-  const uint32_t *R;   // [num_ranges][m]     (kModeRange)
+  const uint32_t *R;     // [num_ranges][m]     (kModeRange)
   const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
   const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
-  uint32_t *hdr;       // [0] key-domain error flag
+  uint32_t *hdr;         // [0] key-domain error flag
   uint32_t *bucket_offsets;
   int mode;
   int use_tma;
 };
 
-// Shared memory carve-up (bytes): 2 stages x (keys [+ values]) | bucket byte per
-// reordered slot | per-warp peer masks [W][m] | per-warp counts [W][m] | delta[m]
-__host__ __device__ constexpr size_t kf_stage_words(bool pairs) {
-  return (size_t)(pairs ? kTilePairs : kTileKeys) * (pairs ? 2u : 1u);
+// CTA shapes (warps W, windows per warp ITEMS; tile T = 32 W ITEMS):
+//   keys, m <= 64 : 16 x 16 (T 8192)    pairs, m <= 64 : 16 x 8 (T 4096)
+//   keys, m >  64 :  8 x 16 (T 4096)    pairs, m >  64 :  8 x 8 (T 2048)
+// chosen so that two (m <= 64) or three (m > 64) CTAs fit in an SM's 228 KB.
+struct KfShape {
+  int warps, items, ctas_per_sm;
+};
+__host__ __device__ constexpr KfShape kf_shape(bool pairs, bool bigm) {
+  return bigm ? KfShape{8, pairs ? 8 : 16, 3} : KfShape{16, pairs ? 8 : 16, 2};
 }
-__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
-  const size_t T = pairs ? kTilePairs : kTileKeys;
-  const size_t mm = m < 2 ? 2 : m;
-  return 2 * kf_stage_words(pairs) * 4 + T + 2 * (size_t)kWarps * mm * 4 + mm * 4;
+__host__ __device__ constexpr uint32_t kf_tile(bool pairs, bool bigm) {
+  return 32u * (uint32_t)kf_shape(pairs, bigm).warps * (uint32_t)kf_shape(pairs, bigm).items;
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, bool FULL>
-__device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
-                                        uint32_t tn, uint32_t *s_keys, uint32_t *s_vals,
-                                        uint8_t *s_bkt, uint32_t *s_mask, uint32_t *s_cnt,
-                                        uint32_t *s_delta, uint32_t *s_wsum, uint32_t &running) {
-  constexpr int ITEMS = TileCfg<PAIRS>::kItems;
-  constexpr uint32_t RE_SMALL = 2;
+// Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
+// | per-warp counts [W][m] | delta[m]
+__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
+  const bool bigm = m > 64;
+  const size_t T = kf_tile(pairs, bigm), W = (size_t)kf_shape(pairs, bigm).warps;
+  const size_t words = T * (pairs ? 2u : 1u);
+  const size_t mm = m < 2 ? 2 : m;
+  return 3 * words * 4 + 3 * W * mm * 4 + mm * 4;
+}
+
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool FULL>
+__device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
+                                           uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
+                                           uint32_t *s_mask, uint32_t *s_cnt, uint32_t *s_delta,
+                                           uint32_t *s_wsum, uint32_t &running) {
+  constexpr uint32_t NT = W * 32;
+  constexpr uint32_t T = NT * ITEMS;
   const uint32_t m = bp.m;
-  const uint32_t re = SMALLM ? RE_SMALL : m;  // counters per warp row
+  const uint32_t re = SMALLM ? 2u : m;  // counters per warp row
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = lanemask_lt(), lanebit = 1u << lane;
   const uint32_t wbase = warp * (ITEMS * 32);
-  uint32_t *mrow = s_mask + warp * re;
   uint32_t *crow = s_cnt + warp * re;
+  uint32_t *mrow0 = s_mask + warp * re;            // window parity 0
+  uint32_t *mrow1 = s_mask + (W + warp) * re;      // window parity 1
+  const uint32_t *in_k = s_in;
+  const uint32_t *in_v = s_in + T;
+  uint32_t *out_k = s_out;
+  uint32_t *out_v = s_out + T;
 
   // ---- 1. warp-level stable ranking, window by window (Eq.4 terms 1-2) ----
+  // Peer masks come from one shared-memory OR of the lane bit per key (the
+  // ballot-based voting of Alg.3, in one instruction); masks are
+  // double-buffered by window parity, so two __syncwarp per window suffice.
   if constexpr (!SMALLM) {
     for (uint32_t j = lane; j < m; j += 32) {
-      mrow[j] = 0u;
+      mrow0[j] = 0u;
+      mrow1[j] = 0u;
       crow[j] = 0u;
     }
-    __syncwarp();
   }
-  uint32_t pk[ITEMS];  // (bucket << 16) | rank within the warp
+  __syncwarp();
+  // rank of each element within its warp (< 32*ITEMS), two 16-bit ranks per
+  // register; the bucket is recomputed from the key when it is reordered
+  uint32_t rk[(ITEMS + 1) / 2];
+#pragma unroll
+  for (int i = 0; i < (ITEMS + 1) / 2; ++i) rk[i] = 0u;
   uint32_t c0 = 0, c1 = 0;
   bool derr = false;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
     const bool valid = FULL || idx < tn;
-    const uint32_t key = valid ? s_keys[idx] : 0u;
+    const uint32_t key = valid ? in_k[idx] : 0u;
     const uint32_t b = bucket_of<KIND>(key, bp);
     if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key, bp);
-    pk[i] = 0u;
     if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: window past the tail
     uint32_t r;
     if constexpr (SMALLM) {
@@ -234,22 +259,20 @@ __device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp,
       c1 += __popc(ones);
       c0 += __popc(zeros);
     } else {
-      // peer mask by shared-memory OR of lane bits (replaces the log2 m ballots of
-      // Alg.3 P:909-930 with one atomic), then rank = warp count + lanes below
+      uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
       if (valid) atomicOr(mrow + b, lanebit);
       __syncwarp();
       const uint32_t peers = valid ? mrow[b] : 0u;
       const uint32_t cnt = valid ? crow[b] : 0u;
       const uint32_t below = peers & lt;
       r = cnt + __popc(below);
-      __syncwarp();
-      if (valid && below == 0u) {  // group leader: clear the mask, advance the count
+      __syncwarp();                // every lane has read before the leader writes
+      if (valid && below == 0u) {  // group leader: clear this parity's mask, advance the count
         mrow[b] = 0u;
         crow[b] = cnt + __popc(peers);
       }
-      __syncwarp();
     }
-    pk[i] = (b << 16) | r;
+    rk[i / 2] |= r << (16 * (i & 1));
   }
   if constexpr (SMALLM) {
     if (lane == 0) {
@@ -266,16 +289,17 @@ __device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp,
   // (Eq.4 term 3 plus the tile's bucket bases: a stable local multisplit of
   // the tile, Sec.4.7 / Sec.5.6.2)
   {
-    const uint32_t total = m * kWarps;
-    const uint32_t per = (total + kThreads - 1) / kThreads;  // <= 8
+    constexpr uint32_t PER_MAX = (kMaxBuckets * W + NT - 1) / NT;  // 8
+    const uint32_t total = m * W;
+    const uint32_t per = (total + NT - 1) / NT;
     const uint32_t q0 = tid * per;
-    uint32_t v[8];
+    uint32_t v[PER_MAX];
     uint32_t s = 0;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < (int)PER_MAX; ++e) {
       const uint32_t q = q0 + (uint32_t)e;
       v[e] = 0u;
-      if ((uint32_t)e < per && q < total) v[e] = s_cnt[(q % kWarps) * re + q / kWarps];
+      if ((uint32_t)e < per && q < total) v[e] = s_cnt[(q % W) * re + q / W];
       s += v[e];
     }
     uint32_t incl = s;
@@ -287,22 +311,22 @@ __device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp,
     if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
+      const uint32_t x = lane < (uint32_t)W ? s_wsum[lane] : 0u;
       uint32_t xi = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, xi, o);
         if (lane >= (uint32_t)o) xi += t;
       }
-      if (lane < (uint32_t)kWarps) s_wsum[lane] = xi - x;
+      if (lane < (uint32_t)W) s_wsum[lane] = xi - x;
     }
     __syncthreads();
     uint32_t run = s_wsum[warp] + incl - s;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < (int)PER_MAX; ++e) {
       const uint32_t q = q0 + (uint32_t)e;
       if ((uint32_t)e < per && q < total) {
-        s_cnt[(q % kWarps) * re + q / kWarps] = run;
+        s_cnt[(q % W) * re + q / W] = run;
         run += v[e];
       }
     }
@@ -329,27 +353,16 @@ __device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp,
     s_delta[tid] = d;
   }
 
-  // ---- 4. reorder the tile in shared memory (stable local multisplit) --------
-  // keys (and values) are re-read in input order into registers only now, so
-  // that the ranking phase holds just the packed ranks
-  uint32_t key[ITEMS];
-  uint32_t val[PAIRS ? ITEMS : 1];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-    key[i] = (FULL || idx < tn) ? s_keys[idx] : 0u;
-    if constexpr (PAIRS) val[i] = (FULL || idx < tn) ? s_vals[idx] : 0u;
-    pk[i] = crow[pk[i] >> 16] + (pk[i] & 0xFFFFu) + (pk[i] & 0xFF0000u) * 256u;  // slot | b << 24
-  }
-  __syncthreads();  // every input-order element is in registers before slots are overwritten
+  // ---- 4. reorder into the output buffer (stable local multisplit) -----------
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
     if (FULL || idx < tn) {
-      const uint32_t slot = pk[i] & 0xFFFFFFu;
-      s_keys[slot] = key[i];
-      s_bkt[slot] = (uint8_t)(pk[i] >> 24);
-      if constexpr (PAIRS) s_vals[slot] = val[i];
+      const uint32_t key = in_k[idx];
+      const uint32_t r = (i & 1) ? (rk[i / 2] >> 16) : (rk[i / 2] & 0xFFFFu);
+      const uint32_t slot = crow[bucket_of<KIND>(key, bp)] + r;
+      out_k[slot] = key;
+      if constexpr (PAIRS) out_v[slot] = in_v[idx];
     }
   }
   __syncthreads();
@@ -357,30 +370,31 @@ __device__ __forceinline__ void kf_tile(const KfArgs &a, const BucketParams &bp,
   // ---- 5. coalesced scatter: slot s of bucket b -> delta[b] + s --------------
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t s = (uint32_t)i * kThreads + tid;
+    const uint32_t s = wbase + (uint32_t)i * 32u + lane;
     if (FULL || s < tn) {
-      const uint32_t p = s_delta[s_bkt[s]] + s;
-      a.keys_out[p] = s_keys[s];
-      if constexpr (PAIRS) a.vals_out[p] = s_vals[s];
+      const uint32_t k = out_k[s];
+      const uint32_t p = s_delta[bucket_of<KIND>(k, bp)] + s;
+      a.keys_out[p] = k;
+      if constexpr (PAIRS) a.vals_out[p] = out_v[s];
     }
   }
-  __syncthreads();
 }
 
-template <int KIND, bool PAIRS, bool SMALLM>
-__global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams bp) {
-  constexpr uint32_t T = TileCfg<PAIRS>::kTile;
-  constexpr uint32_t SW = (uint32_t)kf_stage_words(PAIRS);
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams bp) {
+  constexpr uint32_t NT = W * 32;
+  constexpr uint32_t T = NT * ITEMS;
+  constexpr uint32_t SW = T * (PAIRS ? 2u : 1u);  // words per stage
   extern __shared__ __align__(128) uint8_t kf_smem[];
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_wsum[32];
   const uint32_t m = bp.m;
   const uint32_t mm = m < 2 ? 2 : m;
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
-  uint8_t *s_bkt = kf_smem + 2 * SW * 4;
-  uint32_t *s_mask = reinterpret_cast<uint32_t *>(s_bkt + T);
-  uint32_t *s_cnt = s_mask + kWarps * mm;
-  uint32_t *s_delta = s_cnt + kWarps * mm;
+  uint32_t *s_out = stage0 + 2 * SW;
+  uint32_t *s_mask = s_out + SW;
+  uint32_t *s_cnt = s_mask + 2 * W * mm;
+  uint32_t *s_delta = s_cnt + W * mm;
   const uint32_t tid = threadIdx.x;
 
   uint32_t t0 = 0, t1 = 1;
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams b
     if (tid == 0 && t < t1 && a.use_tma && tile_n(t) == T) {
       uint32_t *dst = stage0 + st * SW;
       const uint64_t pol = policy_evict_first();
-      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
+      mbar_arrive_expect_tx(&bar[st], SW * 4u);
       tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
       if constexpr (PAIRS) tma_load_1d(dst + T, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
     }
@@ -412,12 +426,12 @@ __global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams b
   // thread b < m ends with running = sum_{j<b} total_j + sum_{c<blockIdx} R[c][b]
   uint32_t running = 0;
   if (a.mode == kModeRange) {
-    uint32_t *s_tot = reinterpret_cast<uint32_t *>(s_bkt);  // scratch before the first tile
-    uint32_t *s_pre = s_tot + kThreads;
-    const uint32_t P = kThreads / m;  // row groups (>= 2)
+    uint32_t *s_tot = s_out;  // scratch before the first tile
+    uint32_t *s_pre = s_out + NT;
+    const uint32_t P = NT / m;  // row groups (>= 1)
     const uint32_t b = tid % m, p = tid / m;
-    uint32_t tot = 0, pre = 0;
     if (p < P) {
+      uint32_t tot = 0, pre = 0;
       for (uint32_t r = p; r < a.num_ranges; r += P) {
         const uint32_t v = a.R[(size_t)r * m + b];
         tot += v;
@@ -445,14 +459,14 @@ __global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams b
     if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
+      const uint32_t x = lane < (uint32_t)W ? s_wsum[lane] : 0u;
       uint32_t xi = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
         if (lane >= (uint32_t)o) xi += y;
       }
-      if (lane < (uint32_t)kWarps) s_wsum[lane] = xi - x;
+      if (lane < (uint32_t)W) s_wsum[lane] = xi - x;
     }
     __syncthreads();
     if (tid < m) {
@@ -470,26 +484,27 @@ __global__ void __launch_bounds__(kThreads, 2) kf_fused(KfArgs a, BucketParams b
   uint32_t k = 0;
   for (uint32_t t = t0; t < t1; ++t, ++k) {
     const int st = (int)(k & 1u);
-    uint32_t *s_keys = stage0 + st * SW;
-    uint32_t *s_vals = s_keys + T;
+    uint32_t *s_in = stage0 + st * SW;
     const uint32_t tn = tile_n(t);
     if (a.use_tma && tn == T) {
       mbar_wait(&bar[st], (k >> 1) & 1u);
     } else {  // ragged last tile / unaligned input: plain loads
-      for (uint32_t i = tid; i < tn; i += kThreads) {
-        s_keys[i] = __ldg(a.keys_in + (size_t)t * T + i);
-        if constexpr (PAIRS) s_vals[i] = __ldg(a.vals_in + (size_t)t * T + i);
+      for (uint32_t i = tid; i < tn; i += NT) {
+        s_in[i] = __ldg(a.keys_in + (size_t)t * T + i);
+        if constexpr (PAIRS) s_in[T + i] = __ldg(a.vals_in + (size_t)t * T + i);
       }
       __syncthreads();
     }
     if (tn == T)
-      kf_tile<KIND, PAIRS, SMALLM, true>(a, bp, t, tn, s_keys, s_vals, s_bkt, s_mask, s_cnt,
-                                         s_delta, s_wsum, running);
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, true>(a, bp, t, tn, s_in, s_out, s_mask, s_cnt,
+                                                      s_delta, s_wsum, running);
     else
-      kf_tile<KIND, PAIRS, SMALLM, false>(a, bp, t, tn, s_keys, s_vals, s_bkt, s_mask, s_cnt,
-                                          s_delta, s_wsum, running);
-    if (tid == 0) fence_proxy_async_smem();  // generic-proxy smem writes before the next TMA
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, false>(a, bp, t, tn, s_in, s_out, s_mask, s_cnt,
+                                                       s_delta, s_wsum, running);
+    // the input stage was last read by the reorder (before its barrier): refill it
+    if (tid == 0) fence_proxy_async_smem();
     issue(t + 2, st);
+    __syncthreads();  // the store phase has read s_out / s_delta before the next tile reuses them
   }
 }
 
