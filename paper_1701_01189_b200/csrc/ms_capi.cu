@@ -125,6 +125,11 @@ int sm_count() {
   return n;
 }
 
+bool env_flag(const char *name) {
+  const char *v = std::getenv(name);
+  return v && *v && std::strcmp(v, "0") != 0;
+}
+
 bool three_launch_mode() {
   const char *v = std::getenv("MS_PIPELINE");
   return v && !std::strcmp(v, "3pass");
@@ -206,6 +211,9 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.hdr = hdr;
   a.bucket_offsets = bucket_offsets;
   a.use_tma = (((uintptr_t)keys_in & 15u) == 0) && (!pairs || (((uintptr_t)vals_in & 15u) == 0));
+  // whole-run TMA stores for m <= 64 (long runs); per-element stores beyond
+  a.store_runs = m <= 64 && (((uintptr_t)keys_out & 15u) == 0) &&
+                 (!pairs || (((uintptr_t)vals_out & 15u) == 0)) && !env_flag("MS_NO_RUN_STORES");
 
   if (n <= lo.T) {  // one subproblem: a single launch
     a.mode = kModeSingle;

@@ -175,7 +175,8 @@ struct KfArgs {
   uint32_t *hdr;         // [0] key-domain error flag
   uint32_t *bucket_offsets;
   int mode;
-  int use_tma;
+  int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
+  int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
 };
 
 // CTA shapes (warps W, windows per warp ITEMS; tile T = 32 W ITEMS):
@@ -192,35 +193,65 @@ __host__ __device__ constexpr uint32_t kf_tile(bool pairs, bool bigm) {
   return 32u * (uint32_t)kf_shape(pairs, bigm).warps * (uint32_t)kf_shape(pairs, bigm).items;
 }
 
+// Reordered-tile capacity: T slots plus up to 4m+4 of padding, so that every
+// bucket run can start at the same offset mod 4 as its global destination
+// (16-byte aligned TMA bulk stores of the run body).
+__host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
+  return T + 4u * (m < 2 ? 2u : m) + 4u;
+}
 // Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
 // | per-warp counts [W][m] | delta[m]
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   const bool bigm = m > 64;
   const size_t T = kf_tile(pairs, bigm), W = (size_t)kf_shape(pairs, bigm).warps;
-  const size_t words = T * (pairs ? 2u : 1u);
+  const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  return 3 * words * 4 + 3 * W * mm * 4 + mm * 4;
+  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + mm * 4;
 }
 
 template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool FULL>
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
                                            uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
-                                           uint32_t *s_mask, uint32_t *s_cnt, uint32_t *s_delta,
-                                           uint32_t *s_wsum, uint32_t &running) {
+                                           uint32_t OS, uint32_t *s_mask, uint32_t *s_cnt,
+                                           uint32_t *s_delta, uint32_t *s_wsum,
+                                           uint32_t &running) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
+  constexpr int NB = (ITEMS + 3) / 4;  // registers of packed 8-bit buckets
+  constexpr int NR = (ITEMS + 1) / 2;  // registers of packed 16-bit ranks
   const uint32_t m = bp.m;
   const uint32_t re = SMALLM ? 2u : m;  // counters per warp row
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = lanemask_lt(), lanebit = 1u << lane;
   const uint32_t wbase = warp * (ITEMS * 32);
   uint32_t *crow = s_cnt + warp * re;
-  uint32_t *mrow0 = s_mask + warp * re;            // window parity 0
-  uint32_t *mrow1 = s_mask + (W + warp) * re;      // window parity 1
-  const uint32_t *in_k = s_in;
-  const uint32_t *in_v = s_in + T;
+  uint32_t *mrow0 = s_mask + warp * re;        // window parity 0
+  uint32_t *mrow1 = s_mask + (W + warp) * re;  // window parity 1
+  const uint32_t *in_k = s_in + wbase + lane;  // element i of this lane: in_k[32 i]
+  const uint32_t *in_v = s_in + T + wbase + lane;
   uint32_t *out_k = s_out;
-  uint32_t *out_v = s_out + T;
+  uint32_t *out_v = s_out + OS;
+  auto valid_at = [&](int i) { return FULL || wbase + (uint32_t)i * 32u + lane < tn; };
+
+  // ---- 0. buckets of this lane's ITEMS elements (all loads issued together) ----
+  uint32_t bk[NB];
+  bool derr = false;
+  // ITEMS <= 8: the keys stay in registers until the reorder; otherwise they
+  // are re-read there (keeps the 16-item ranking loop within 64 registers)
+  constexpr bool KEEP = ITEMS <= 8;
+  uint32_t key[ITEMS];
+  {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = valid_at(i) ? in_k[32 * i] : 0u;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) bk[j] = 0u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      bk[i / 4] |= bucket_of<KIND>(key[i], bp) << (8 * (i & 3));
+      if constexpr (KIND == kIdentity) derr |= valid_at(i) && key_domain_error<KIND>(key[i], bp);
+    }
+  }
+  auto bucket_at = [&](int i) { return (bk[i / 4] >> (8 * (i & 3))) & 0xFFu; };
 
   // ---- 1. warp-level stable ranking, window by window (Eq.4 terms 1-2) ----
   // Peer masks come from one shared-memory OR of the lane bit per key (the
@@ -234,21 +265,15 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     }
   }
   __syncwarp();
-  // rank of each element within its warp (< 32*ITEMS), two 16-bit ranks per
-  // register; the bucket is recomputed from the key when it is reordered
-  uint32_t rk[(ITEMS + 1) / 2];
+  uint32_t rk[NR];  // rank within the warp (< 32 ITEMS), two 16-bit ranks per register
 #pragma unroll
-  for (int i = 0; i < (ITEMS + 1) / 2; ++i) rk[i] = 0u;
+  for (int j = 0; j < NR; ++j) rk[j] = 0u;
   uint32_t c0 = 0, c1 = 0;
-  bool derr = false;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-    const bool valid = FULL || idx < tn;
-    const uint32_t key = valid ? in_k[idx] : 0u;
-    const uint32_t b = bucket_of<KIND>(key, bp);
-    if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key, bp);
+    const bool valid = valid_at(i);
     if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: window past the tail
+    const uint32_t b = bucket_at(i);
     uint32_t r;
     if constexpr (SMALLM) {
       // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
@@ -287,21 +312,13 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
 
   // ---- 2. tile exclusive scan of the counts in (bucket, warp) order ----------
   // (Eq.4 term 3 plus the tile's bucket bases: a stable local multisplit of
-  // the tile, Sec.4.7 / Sec.5.6.2)
+  // the tile, Sec.4.7 / Sec.5.6.2).  Entry q = b*W + w lives at s_cnt[w*re + b].
   {
-    constexpr uint32_t PER_MAX = (kMaxBuckets * W + NT - 1) / NT;  // 8
     const uint32_t total = m * W;
     const uint32_t per = (total + NT - 1) / NT;
-    const uint32_t q0 = tid * per;
-    uint32_t v[PER_MAX];
+    const uint32_t q0 = tid * per, q1 = min(total, q0 + per);
     uint32_t s = 0;
-#pragma unroll
-    for (int e = 0; e < (int)PER_MAX; ++e) {
-      const uint32_t q = q0 + (uint32_t)e;
-      v[e] = 0u;
-      if ((uint32_t)e < per && q < total) v[e] = s_cnt[(q % W) * re + q / W];
-      s += v[e];
-    }
+    for (uint32_t q = q0; q < q1; ++q) s += s_cnt[(q % W) * re + q / W];
     uint32_t incl = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -322,60 +339,113 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     }
     __syncthreads();
     uint32_t run = s_wsum[warp] + incl - s;
-#pragma unroll
-    for (int e = 0; e < (int)PER_MAX; ++e) {
-      const uint32_t q = q0 + (uint32_t)e;
-      if ((uint32_t)e < per && q < total) {
-        s_cnt[(q % W) * re + q / W] = run;
-        run += v[e];
-      }
+    for (uint32_t q = q0; q < q1; ++q) {
+      uint32_t *c = s_cnt + (q % W) * re + q / W;
+      const uint32_t v = *c;
+      *c = run;
+      run += v;
     }
+    if (a.store_runs && tid < m) bulk_wait_read();  // previous tile's run stores left s_out
   }
   __syncthreads();
 
-  // ---- 3. per bucket: global start of this tile's run (Eq.2/3 terms 1-2) -----
+  // ---- 3. per bucket: global start gs of this tile's run (Eq.2/3 terms 1-2) --
+  // With run stores, bucket b's run is placed at smem offset tb + adj with
+  // adj = 4b + ((gs - tb) mod 4), congruent to gs mod 4 (runs cannot overlap).
+  uint32_t r_start = 0, r_len = 0, r_gs = 0;  // thread b < m: this tile's run of bucket b
   if (tid < m) {
     const uint32_t tb = s_cnt[tid];  // warp 0 row = tile bucket base
     const uint32_t te = tid + 1 < m ? s_cnt[tid + 1] : tn;
-    uint32_t d;
+    uint32_t gs;
     if (a.mode == kModeSingle) {
-      d = 0u;
+      gs = tb;
       if (a.bucket_offsets) {
         a.bucket_offsets[tid] = tb;
         if (tid == m - 1) a.bucket_offsets[m] = tn;
       }
     } else if (a.mode == kModeTileG) {
-      d = a.Gt[(size_t)tile * m + tid] + a.base[tid] - tb;
+      gs = a.Gt[(size_t)tile * m + tid] + a.base[tid];
     } else {
-      d = running - tb;
+      gs = running;
       running += te - tb;
     }
-    s_delta[tid] = d;
+    if (a.store_runs) {
+      const uint32_t adj = 4u * tid + ((gs - tb) & 3u);
+      r_start = tb + adj;
+      r_len = te - tb;
+      r_gs = gs;
+      if (adj)
+        for (uint32_t w = 0; w < (uint32_t)W; ++w) s_cnt[w * re + tid] += adj;
+    } else {
+      s_delta[tid] = gs - tb;
+    }
   }
+  if (a.store_runs) __syncthreads();  // shifted bucket bases are visible to the reorder
 
   // ---- 4. reorder into the output buffer (stable local multisplit) -----------
+  {
+    uint32_t slot[ITEMS];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t idx = wbase + (uint32_t)i * 32u + lane;
-    if (FULL || idx < tn) {
-      const uint32_t key = in_k[idx];
-      const uint32_t r = (i & 1) ? (rk[i / 2] >> 16) : (rk[i / 2] & 0xFFFFu);
-      const uint32_t slot = crow[bucket_of<KIND>(key, bp)] + r;
-      out_k[slot] = key;
-      if constexpr (PAIRS) out_v[slot] = in_v[idx];
+    for (int i = 0; i < ITEMS; ++i)
+      slot[i] = crow[bucket_at(i)] + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
+    if constexpr (!KEEP) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) key[i] = in_k[32 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (valid_at(i)) out_k[slot[i]] = key[i];
+    if constexpr (PAIRS) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) key[i] = in_v[32 * i];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (valid_at(i)) out_v[slot[i]] = key[i];
     }
   }
   __syncthreads();
 
+  if (a.store_runs) {
+    // ---- 5a. one TMA bulk store per bucket run (16-byte aligned body), the
+    //          <= 3 leading and trailing elements with plain stores
+    if (tid < m && r_len > 0) {
+      const uint32_t head = min(r_len, (4u - (r_gs & 3u)) & 3u);
+      const uint32_t body = (r_len - head) & ~3u;
+      for (uint32_t j = 0; j < head; ++j) {
+        a.keys_out[r_gs + j] = out_k[r_start + j];
+        if constexpr (PAIRS) a.vals_out[r_gs + j] = out_v[r_start + j];
+      }
+      for (uint32_t j = head + body; j < r_len; ++j) {
+        a.keys_out[r_gs + j] = out_k[r_start + j];
+        if constexpr (PAIRS) a.vals_out[r_gs + j] = out_v[r_start + j];
+      }
+      if (body) {
+        fence_proxy_async_smem();
+        tma_store_1d(a.keys_out + r_gs + head, out_k + r_start + head, body * 4u);
+        if constexpr (PAIRS) tma_store_1d(a.vals_out + r_gs + head, out_v + r_start + head, body * 4u);
+        bulk_commit();
+      }
+    }
+    return;
+  }
+
   // ---- 5. coalesced scatter: slot s of bucket b -> delta[b] + s --------------
+  {
+    const uint32_t s0 = wbase + lane;
+    uint32_t key[ITEMS], pos[ITEMS];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t s = wbase + (uint32_t)i * 32u + lane;
-    if (FULL || s < tn) {
-      const uint32_t k = out_k[s];
-      const uint32_t p = s_delta[bucket_of<KIND>(k, bp)] + s;
-      a.keys_out[p] = k;
-      if constexpr (PAIRS) a.vals_out[p] = out_v[s];
+    for (int i = 0; i < ITEMS; ++i) key[i] = out_k[s0 + 32 * i];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) pos[i] = s_delta[bucket_of<KIND>(key[i], bp)] + s0 + 32 * i;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (valid_at(i)) a.keys_out[pos[i]] = key[i];
+    if constexpr (PAIRS) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) key[i] = out_v[s0 + 32 * i];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (valid_at(i)) a.vals_out[pos[i]] = key[i];
     }
   }
 }
@@ -390,9 +460,10 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   __shared__ uint32_t s_wsum[32];
   const uint32_t m = bp.m;
   const uint32_t mm = m < 2 ? 2 : m;
+  const uint32_t OS = kf_out_slots(T, m);
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
   uint32_t *s_out = stage0 + 2 * SW;
-  uint32_t *s_mask = s_out + SW;
+  uint32_t *s_mask = s_out + OS * (PAIRS ? 2u : 1u);
   uint32_t *s_cnt = s_mask + 2 * W * mm;
   uint32_t *s_delta = s_cnt + W * mm;
   const uint32_t tid = threadIdx.x;
@@ -432,8 +503,9 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     const uint32_t b = tid % m, p = tid / m;
     if (p < P) {
       uint32_t tot = 0, pre = 0;
+#pragma unroll 8
       for (uint32_t r = p; r < a.num_ranges; r += P) {
-        const uint32_t v = a.R[(size_t)r * m + b];
+        const uint32_t v = __ldg(a.R + (size_t)r * m + b);
         tot += v;
         pre += r < blockIdx.x ? v : 0u;
       }
@@ -496,16 +568,17 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       __syncthreads();
     }
     if (tn == T)
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, true>(a, bp, t, tn, s_in, s_out, s_mask, s_cnt,
-                                                      s_delta, s_wsum, running);
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+                                                      s_cnt, s_delta, s_wsum, running);
     else
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, false>(a, bp, t, tn, s_in, s_out, s_mask, s_cnt,
-                                                       s_delta, s_wsum, running);
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+                                                       s_cnt, s_delta, s_wsum, running);
     // the input stage was last read by the reorder (before its barrier): refill it
     if (tid == 0) fence_proxy_async_smem();
     issue(t + 2, st);
     __syncthreads();  // the store phase has read s_out / s_delta before the next tile reuses them
   }
+  if (a.store_runs && tid < m) bulk_wait_all();  // run stores complete before smem is released
 }
 
 }  // namespace ms

@@ -116,6 +116,30 @@ def test_unaligned_inputs(kind):
     assert np.array_equal(host(off), eo)
 
 
+@pytest.mark.parametrize("m", [2, 37, 64])
+def test_unaligned_outputs(m):
+    # outputs not 16-byte aligned disable the whole-run TMA stores
+    ob, pb, gk = bucket_pair("delta", m)
+    n = 5 * T + 19
+    keys = gen.keys(n, seed=8, dist=gen.DIST_SKEW, **gk)
+    vals = gen.values(n, seed=8)
+    ko = torch.empty(n + 3, dtype=torch.int32, device="cuda")[3:]
+    vo = torch.empty(n + 1, dtype=torch.int32, device="cuda")[1:]
+    ms.multisplit(dev(keys), dev(vals), bucket=pb, out_keys=ko, out_values=vo)
+    ek, ev, _ = oracle.multisplit(keys, ob, vals)
+    assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev)
+
+
+def test_per_element_store_path(monkeypatch):
+    monkeypatch.setenv("MS_NO_RUN_STORES", "1")
+    for m in (2, 32):
+        ob, pb, gk = bucket_pair("delta", m)
+        n = 7 * T + 5
+        keys = gen.keys(n, seed=m, dist=gen.DIST_BINOMIAL, **gk)
+        check_multisplit(keys, gen.values(n, seed=1), ob, pb)
+        check_multisplit(keys, None, ob, pb)
+
+
 def test_custom_delta_widths():
     for m, d in ((7, 1), (7, 3), (100, 12345), (256, 2**24 + 7), (3, 2**31 + 1)):
         ob, pb = oracle.delta(m, d), ms.Delta(m, d)
