@@ -197,7 +197,7 @@ __host__ __device__ constexpr uint32_t kf_tile(bool pairs, bool bigm) {
 // bucket run can start at the same offset mod 4 as its global destination
 // (16-byte aligned TMA bulk stores of the run body).
 __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
-  return T + 4u * (m < 2 ? 2u : m) + 4u;
+  return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;  // m > 64 never uses run stores
 }
 // Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
 // | per-warp counts [W][m] | delta[m]
@@ -353,30 +353,37 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   // With run stores, bucket b's run is placed at smem offset tb + adj with
   // adj = 4b + ((gs - tb) mod 4), congruent to gs mod 4 (runs cannot overlap).
   uint32_t r_start = 0, r_len = 0, r_gs = 0;  // thread b < m: this tile's run of bucket b
-  if (tid < m) {
-    const uint32_t tb = s_cnt[tid];  // warp 0 row = tile bucket base
-    const uint32_t te = tid + 1 < m ? s_cnt[tid + 1] : tn;
-    uint32_t gs;
-    if (a.mode == kModeSingle) {
-      gs = tb;
-      if (a.bucket_offsets) {
-        a.bucket_offsets[tid] = tb;
-        if (tid == m - 1) a.bucket_offsets[m] = tn;
+  const uint32_t mw = (m + 31u) & ~31u;       // warps holding the m bucket threads
+  if (tid < mw) {
+    uint32_t tb = 0, te = 0, gs = 0;
+    if (tid < m) {
+      tb = s_cnt[tid];  // warp 0 row = tile bucket base
+      te = tid + 1 < m ? s_cnt[tid + 1] : tn;
+      if (a.mode == kModeSingle) {
+        gs = tb;
+        if (a.bucket_offsets) {
+          a.bucket_offsets[tid] = tb;
+          if (tid == m - 1) a.bucket_offsets[m] = tn;
+        }
+      } else if (a.mode == kModeTileG) {
+        gs = a.Gt[(size_t)tile * m + tid] + a.base[tid];
+      } else {
+        gs = running;
+        running += te - tb;
       }
-    } else if (a.mode == kModeTileG) {
-      gs = a.Gt[(size_t)tile * m + tid] + a.base[tid];
-    } else {
-      gs = running;
-      running += te - tb;
     }
     if (a.store_runs) {
-      const uint32_t adj = 4u * tid + ((gs - tb) & 3u);
-      r_start = tb + adj;
-      r_len = te - tb;
-      r_gs = gs;
-      if (adj)
-        for (uint32_t w = 0; w < (uint32_t)W; ++w) s_cnt[w * re + tid] += adj;
-    } else {
+      // every bucket thread has read its neighbour's base before any is shifted
+      if (mw > 32) named_barrier_sync(1, mw); else __syncwarp();
+      if (tid < m) {
+        const uint32_t adj = 4u * tid + ((gs - tb) & 3u);
+        r_start = tb + adj;
+        r_len = te - tb;
+        r_gs = gs;
+        if (adj)
+          for (uint32_t w = 0; w < (uint32_t)W; ++w) s_cnt[w * re + tid] += adj;
+      }
+    } else if (tid < m) {
       s_delta[tid] = gs - tb;
     }
   }
