@@ -200,21 +200,21 @@ __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
   return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;  // m > 64 never uses run stores
 }
 // Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
-// | per-warp counts [W][m] | delta[m]
+// | per-warp counts [W][m] | delta[m] | run table [3][m]
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   const bool bigm = m > 64;
   const size_t T = kf_tile(pairs, bigm), W = (size_t)kf_shape(pairs, bigm).warps;
   const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + mm * 4;
+  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + 4 * mm * 4;
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool FULL>
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool FULL, class OnInputFree>
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
                                            uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
                                            uint32_t OS, uint32_t *s_mask, uint32_t *s_cnt,
-                                           uint32_t *s_delta, uint32_t *s_wsum,
-                                           uint32_t &running) {
+                                           uint32_t *s_delta, uint32_t *s_run, uint32_t *s_wsum,
+                                           uint32_t &running, OnInputFree on_input_free) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
   constexpr int NB = (ITEMS + 3) / 4;  // registers of packed 8-bit buckets
@@ -380,6 +380,9 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
         r_start = tb + adj;
         r_len = te - tb;
         r_gs = gs;
+        s_run[tid] = r_start;
+        s_run[m + tid] = r_gs;
+        s_run[2 * m + tid] = r_len;
         if (adj)
           for (uint32_t w = 0; w < (uint32_t)W; ++w) s_cnt[w * re + tid] += adj;
       }
@@ -412,25 +415,37 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   }
   __syncthreads();
 
+  on_input_free();  // the input stage has been read for the last time
+
   if (a.store_runs) {
-    // ---- 5a. one TMA bulk store per bucket run (16-byte aligned body), the
-    //          <= 3 leading and trailing elements with plain stores
+    // ---- 5a. one TMA bulk store per bucket run: the 16-byte aligned body by
+    //          thread b, the <= 3 leading / trailing elements by threads 8b..8b+7
     if (tid < m && r_len > 0) {
       const uint32_t head = min(r_len, (4u - (r_gs & 3u)) & 3u);
       const uint32_t body = (r_len - head) & ~3u;
-      for (uint32_t j = 0; j < head; ++j) {
-        a.keys_out[r_gs + j] = out_k[r_start + j];
-        if constexpr (PAIRS) a.vals_out[r_gs + j] = out_v[r_start + j];
-      }
-      for (uint32_t j = head + body; j < r_len; ++j) {
-        a.keys_out[r_gs + j] = out_k[r_start + j];
-        if constexpr (PAIRS) a.vals_out[r_gs + j] = out_v[r_start + j];
-      }
       if (body) {
         fence_proxy_async_smem();
         tma_store_1d(a.keys_out + r_gs + head, out_k + r_start + head, body * 4u);
         if constexpr (PAIRS) tma_store_1d(a.vals_out + r_gs + head, out_v + r_start + head, body * 4u);
         bulk_commit();
+      }
+    }
+    if (tid < 8u * m) {
+      const uint32_t b = tid >> 3, j = tid & 7u;
+      const uint32_t len = s_run[2 * m + b];
+      const uint32_t gs = s_run[m + b];
+      const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+      const uint32_t tail = (len - head) & 3u;
+      uint32_t e = 0xFFFFFFFFu;  // run-relative element this thread stores, if any
+      if (j < 4u) {
+        if (j < head) e = j;
+      } else if (j - 4u < tail) {
+        e = len - tail + (j - 4u);
+      }
+      if (e != 0xFFFFFFFFu) {
+        const uint32_t st = s_run[b] + e;
+        a.keys_out[gs + e] = out_k[st];
+        if constexpr (PAIRS) a.vals_out[gs + e] = out_v[st];
       }
     }
     return;
@@ -473,7 +488,9 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t *s_mask = s_out + OS * (PAIRS ? 2u : 1u);
   uint32_t *s_cnt = s_mask + 2 * W * mm;
   uint32_t *s_delta = s_cnt + W * mm;
+  uint32_t *s_run = s_delta + mm;
   const uint32_t tid = threadIdx.x;
+  constexpr uint32_t kProducer = NT - 32;  // lane 0 of the last warp issues the TMA loads
 
   uint32_t t0 = 0, t1 = 1;
   if (a.mode != kModeSingle) {
@@ -483,7 +500,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   }
   auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
   auto issue = [&](uint32_t t, int st) {  // one elected thread starts the TMA bulk copy
-    if (tid == 0 && t < t1 && a.use_tma && tile_n(t) == T) {
+    if (tid == kProducer && t < t1 && a.use_tma && tile_n(t) == T) {
       uint32_t *dst = stage0 + st * SW;
       const uint64_t pol = policy_evict_first();
       mbar_arrive_expect_tx(&bar[st], SW * 4u);
@@ -574,16 +591,23 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       }
       __syncthreads();
     }
+    // the producer refills this stage with tile t+2 as soon as it has been read
+    auto refill = [&]() {
+      if (tid == kProducer) {
+        fence_proxy_async_smem();  // generic-proxy smem accesses before the async-proxy write
+        issue(t + 2, st);
+      }
+    };
     if (tn == T)
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                      s_cnt, s_delta, s_wsum, running);
+                                                      s_cnt, s_delta, s_run, s_wsum, running,
+                                                      refill);
     else
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                       s_cnt, s_delta, s_wsum, running);
-    // the input stage was last read by the reorder (before its barrier): refill it
-    if (tid == 0) fence_proxy_async_smem();
-    issue(t + 2, st);
-    __syncthreads();  // the store phase has read s_out / s_delta before the next tile reuses them
+                                                       s_cnt, s_delta, s_run, s_wsum, running,
+                                                       refill);
+    // no CTA barrier here: the next tile's shared structures are first written
+    // after barriers that every thread reaches only once done with this tile
   }
   if (a.store_runs && tid < m) bulk_wait_all();  // run stores complete before smem is released
 }
