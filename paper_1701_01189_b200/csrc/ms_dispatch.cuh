@@ -46,7 +46,7 @@ cudaError_t Launch<KIND>::tile_hist(const uint32_t *keys, uint32_t n, uint32_t t
 template <int KIND, bool PAIRS, bool SMALLM, bool BIGM>
 static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
   constexpr KfShape sh = kf_shape(PAIRS, BIGM);
-  auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm>;
+  auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm, !BIGM>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

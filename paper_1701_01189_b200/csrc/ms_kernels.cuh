@@ -209,12 +209,17 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + 4 * mm * 4;
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool FULL, class OnInputFree>
+// WSCAN (m <= 64 shapes): every warp scans the m x W tile counts itself, so a
+// tile needs two CTA barriers (after ranking, after reordering); otherwise a
+// block-wide scan.  running[k] = next global position of bucket lane + 32k
+// (WSCAN) or of bucket tid (block scan).
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool WSCAN, bool FULL,
+          class OnInputFree>
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
                                            uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
                                            uint32_t OS, uint32_t *s_mask, uint32_t *s_cnt,
                                            uint32_t *s_delta, uint32_t *s_run, uint32_t *s_wsum,
-                                           uint32_t &running, OnInputFree on_input_free) {
+                                           uint32_t (&running)[2], OnInputFree on_input_free) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
   constexpr int NB = (ITEMS + 3) / 4;  // registers of packed 8-bit buckets
@@ -308,8 +313,69 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if constexpr (KIND == kIdentity) {
     if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
   }
+  if (WSCAN && a.store_runs && warp == 0) bulk_wait_read();  // previous run stores left s_out
   __syncthreads();
 
+  if constexpr (WSCAN) {
+    // ---- 2'/3'. per-warp scan: this warp's slot base for bucket b is
+    //   tile base tb[b] (buckets before b) + counts of b in warps before this one
+    //   (Eq.4 terms 2-3), plus the run padding adj[b] (run stores).
+    uint32_t colp[2] = {0u, 0u}, tot[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t b = lane + 32u * (uint32_t)k;
+      if (b < m) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint32_t c = s_cnt[w * re + b];
+          tot[k] += c;
+          colp[k] += ((uint32_t)w < warp) ? c : 0u;
+        }
+      }
+    }
+    uint32_t incl[2] = {tot[0], tot[1]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl[k], o);
+        if (lane >= (uint32_t)o) incl[k] += t;
+      }
+    }
+    const uint32_t sum0 = __shfl_sync(0xFFFFFFFFu, incl[0], 31);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t b = lane + 32u * (uint32_t)k;
+      if (b < m) {
+        const uint32_t tb = incl[k] - tot[k] + (k ? sum0 : 0u);
+        uint32_t gs;
+        if (a.mode == kModeSingle) {
+          gs = tb;
+          if (warp == 0 && a.bucket_offsets) {
+            a.bucket_offsets[b] = tb;
+            if (b == m - 1) a.bucket_offsets[m] = tn;
+          }
+        } else if (a.mode == kModeTileG) {
+          gs = a.Gt[(size_t)tile * m + b] + a.base[b];
+        } else {
+          gs = running[k];
+          running[k] += tot[k];
+        }
+        const uint32_t adj = a.store_runs ? 4u * b + ((gs - tb) & 3u) : 0u;
+        mrow0[b] = tb + colp[k] + adj;  // mask row 0 is free after ranking
+        if (warp == 0) {
+          if (a.store_runs) {
+            s_run[b] = tb + adj;
+            s_run[m + b] = gs;
+            s_run[2 * m + b] = tot[k];
+          } else {
+            s_delta[b] = gs - tb;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
   // ---- 2. tile exclusive scan of the counts in (bucket, warp) order ----------
   // (Eq.4 term 3 plus the tile's bucket bases: a stable local multisplit of
   // the tile, Sec.4.7 / Sec.5.6.2).  Entry q = b*W + w lives at s_cnt[w*re + b].
@@ -345,14 +411,13 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       *c = run;
       run += v;
     }
-    if (a.store_runs && tid < m) bulk_wait_read();  // previous tile's run stores left s_out
+    if (a.store_runs && warp == 0) bulk_wait_read();  // previous tile's run stores left s_out
   }
   __syncthreads();
 
   // ---- 3. per bucket: global start gs of this tile's run (Eq.2/3 terms 1-2) --
   // With run stores, bucket b's run is placed at smem offset tb + adj with
   // adj = 4b + ((gs - tb) mod 4), congruent to gs mod 4 (runs cannot overlap).
-  uint32_t r_start = 0, r_len = 0, r_gs = 0;  // thread b < m: this tile's run of bucket b
   const uint32_t mw = (m + 31u) & ~31u;       // warps holding the m bucket threads
   if (tid < mw) {
     uint32_t tb = 0, te = 0, gs = 0;
@@ -368,8 +433,8 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       } else if (a.mode == kModeTileG) {
         gs = a.Gt[(size_t)tile * m + tid] + a.base[tid];
       } else {
-        gs = running;
-        running += te - tb;
+        gs = running[0];
+        running[0] += te - tb;
       }
     }
     if (a.store_runs) {
@@ -377,12 +442,9 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       if (mw > 32) named_barrier_sync(1, mw); else __syncwarp();
       if (tid < m) {
         const uint32_t adj = 4u * tid + ((gs - tb) & 3u);
-        r_start = tb + adj;
-        r_len = te - tb;
-        r_gs = gs;
-        s_run[tid] = r_start;
-        s_run[m + tid] = r_gs;
-        s_run[2 * m + tid] = r_len;
+        s_run[tid] = tb + adj;
+        s_run[m + tid] = gs;
+        s_run[2 * m + tid] = te - tb;
         if (adj)
           for (uint32_t w = 0; w < (uint32_t)W; ++w) s_cnt[w * re + tid] += adj;
       }
@@ -391,13 +453,16 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     }
   }
   if (a.store_runs) __syncthreads();  // shifted bucket bases are visible to the reorder
+  }  // block scan
+
+  const uint32_t *brow = WSCAN ? mrow0 : crow;  // this warp's slot base per bucket
 
   // ---- 4. reorder into the output buffer (stable local multisplit) -----------
   {
     uint32_t slot[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
-      slot[i] = crow[bucket_at(i)] + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
+      slot[i] = brow[bucket_at(i)] + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
     if constexpr (!KEEP) {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) key[i] = in_k[32 * i];
@@ -420,15 +485,23 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if (a.store_runs) {
     // ---- 5a. one TMA bulk store per bucket run: the 16-byte aligned body by
     //          thread b, the <= 3 leading / trailing elements by threads 8b..8b+7
-    if (tid < m && r_len > 0) {
-      const uint32_t head = min(r_len, (4u - (r_gs & 3u)) & 3u);
-      const uint32_t body = (r_len - head) & ~3u;
-      if (body) {
-        fence_proxy_async_smem();
-        tma_store_1d(a.keys_out + r_gs + head, out_k + r_start + head, body * 4u);
-        if constexpr (PAIRS) tma_store_1d(a.vals_out + r_gs + head, out_v + r_start + head, body * 4u);
-        bulk_commit();
+    // run bodies: one TMA bulk store per bucket, issued by warp 0 (lane b, b + 32)
+    if (warp == 0) {
+      bool issued = false;
+      for (uint32_t b = lane; b < m; b += 32) {
+        const uint32_t len = s_run[2 * m + b];
+        const uint32_t gs = s_run[m + b];
+        const uint32_t st = s_run[b];
+        const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+        const uint32_t body = (len - head) & ~3u;
+        if (body) {
+          fence_proxy_async_smem();
+          tma_store_1d(a.keys_out + gs + head, out_k + st + head, body * 4u);
+          if constexpr (PAIRS) tma_store_1d(a.vals_out + gs + head, out_v + st + head, body * 4u);
+          issued = true;
+        }
       }
+      if (issued) bulk_commit();
     }
     if (tid < 8u * m) {
       const uint32_t b = tid >> 3, j = tid & 7u;
@@ -472,7 +545,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   }
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB>
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB, bool WSCAN>
 __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams bp) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
@@ -519,7 +592,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
 
   // ---- level-0 scan (Eq.3 terms 1-2 over the m x G matrix R) -------------------
   // thread b < m ends with running = sum_{j<b} total_j + sum_{c<blockIdx} R[c][b]
-  uint32_t running = 0;
+  uint32_t running[2] = {0u, 0u};
   if (a.mode == kModeRange) {
     uint32_t *s_tot = s_out;  // scratch before the first tile
     uint32_t *s_pre = s_out + NT;
@@ -567,13 +640,19 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     __syncthreads();
     if (tid < m) {
       const uint32_t gbase = s_wsum[warp] + incl - t;
-      running = gbase + pr;
+      running[0] = gbase + pr;
+      s_delta[tid] = running[0];
       if (blockIdx.x == 0 && a.bucket_offsets) {
         a.bucket_offsets[tid] = gbase;
         if (tid == m - 1) a.bucket_offsets[m] = gbase + t;
       }
     }
     __syncthreads();
+    if constexpr (WSCAN) {  // every warp keeps the offsets of buckets lane, lane + 32
+      const uint32_t lane_ = tid & 31;
+      running[0] = lane_ < m ? s_delta[lane_] : 0u;
+      running[1] = lane_ + 32 < m ? s_delta[lane_ + 32] : 0u;
+    }
   }
 
   // ---- tiles of this range, in order, double-buffered TMA ----------------------
@@ -599,17 +678,17 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       }
     };
     if (tn == T)
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, WSCAN, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
                                                       s_cnt, s_delta, s_run, s_wsum, running,
                                                       refill);
     else
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, WSCAN, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
                                                        s_cnt, s_delta, s_run, s_wsum, running,
                                                        refill);
     // no CTA barrier here: the next tile's shared structures are first written
     // after barriers that every thread reaches only once done with this tile
   }
-  if (a.store_runs && tid < m) bulk_wait_all();  // run stores complete before smem is released
+  if (a.store_runs) bulk_wait_all();  // run stores complete before smem is released
 }
 
 }  // namespace ms
