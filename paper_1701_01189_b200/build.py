@@ -16,7 +16,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-re
          "-I", os.path.join(ROOT, "include")]
 
 SOURCES = ["ms_capi.cu", "ms_inst_identity.cu", "ms_inst_delta.cu", "ms_inst_radix.cu",
-           "ms_inst_deltashift.cu"]
+           "ms_inst_deltashift.cu", "ms_inst_topbits.cu"]
 HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_dispatch.cuh", "ms_scan.cuh"]
 
 

@@ -96,15 +96,16 @@ Plan make_plan(const ms_bucket_fn *fn) {
   switch (fn->kind) {
     case MS_BUCKET_IDENTITY: pl.kind = kIdentity; break;
     case MS_BUCKET_RADIX:
-      pl.kind = kRadix;
+      pl.kind = fn->shift + fn->bits == 32 ? kTopBits : kRadix;
       p.shift = fn->shift;
       p.mask = (1u << fn->bits) - 1u;
       break;
     default: {
       const uint32_t d = fn->delta;
       if ((d & (d - 1u)) == 0u) {  // power of two, including delta = 1
-        pl.kind = kDeltaShift;
         p.shift = (uint32_t)__builtin_ctz(d);
+        // m * delta >= 2^32: u >> shift < m already, no clamp needed
+        pl.kind = ((uint64_t)p.m << p.shift) >= (1ull << 32) ? kTopBits : kDeltaShift;
       } else {
         pl.kind = kDelta;
         // M = ceil(2^64 / delta) = floor((2^64 - 1) / delta) + 1   (delta >= 3 here)
@@ -148,6 +149,7 @@ cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_
     case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
     case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
     case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
     default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
   }
 }
@@ -158,6 +160,7 @@ cudaError_t tile_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t
     case kIdentity: return Launch<kIdentity>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
     case kDelta: return Launch<kDelta>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
     case kRadix: return Launch<kRadix>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
+    case kTopBits: return Launch<kTopBits>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
     default: return Launch<kDeltaShift>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
   }
 }
@@ -167,6 +170,7 @@ cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cu
     case kIdentity: return Launch<kIdentity>::fused(pairs, a, pl.bp, grid, s);
     case kDelta: return Launch<kDelta>::fused(pairs, a, pl.bp, grid, s);
     case kRadix: return Launch<kRadix>::fused(pairs, a, pl.bp, grid, s);
+    case kTopBits: return Launch<kTopBits>::fused(pairs, a, pl.bp, grid, s);
     default: return Launch<kDeltaShift>::fused(pairs, a, pl.bp, grid, s);
   }
 }

@@ -17,9 +17,18 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / kWarp;
 constexpr int kMaxBuckets = 256;
 
-// kDeltaShift is the internal form of DELTA when delta = 2^shift: floor(u/delta)
-// is a shift (the bench's equal-width buckets of P:1107 with m = 2^k).
-enum BucketKind : uint32_t { kIdentity = 0, kDelta = 1, kRadix = 2, kDeltaShift = 3 };
+// Internal forms: kDeltaShift is DELTA with delta = 2^shift (floor(u/delta) is a
+// shift, then the clamp to m-1); kTopBits is f(u) = u >> shift with no clamp or
+// mask, used when the digit is the key's top bits: DELTA with m * 2^shift =
+// 2^32 (the bench's equal-width buckets of P:1107 with m = 2^k) and RADIX
+// with shift + bits = 32 (the last LSD pass).
+enum BucketKind : uint32_t {
+  kIdentity = 0,
+  kDelta = 1,
+  kRadix = 2,
+  kDeltaShift = 3,
+  kTopBits = 4
+};
 
 // Bucket identifier parameters, precomputed on the host.
 struct BucketParams {
@@ -41,6 +50,8 @@ template <int KIND>
 __device__ __forceinline__ uint32_t bucket_of(uint32_t u, const BucketParams &p) {
   if constexpr (KIND == kRadix) {
     return (u >> p.shift) & p.mask;
+  } else if constexpr (KIND == kTopBits) {
+    return u >> p.shift;
   } else if constexpr (KIND == kDeltaShift) {
     const uint32_t q = u >> p.shift;
     return q < p.m1 ? q : p.m1;

@@ -238,30 +238,12 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   uint32_t *out_v = s_out + OS;
   auto valid_at = [&](int i) { return FULL || wbase + (uint32_t)i * 32u + lane < tn; };
 
-  // ---- 0. buckets of this lane's ITEMS elements (all loads issued together) ----
-  uint32_t bk[NB];
-  bool derr = false;
-  // ITEMS <= 8: the keys stay in registers until the reorder; otherwise they
-  // are re-read there (keeps the 16-item ranking loop within 64 registers)
-  constexpr bool KEEP = ITEMS <= 8;
-  uint32_t key[ITEMS];
-  {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) key[i] = valid_at(i) ? in_k[32 * i] : 0u;
-#pragma unroll
-    for (int j = 0; j < NB; ++j) bk[j] = 0u;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      bk[i / 4] |= bucket_of<KIND>(key[i], bp) << (8 * (i & 3));
-      if constexpr (KIND == kIdentity) derr |= valid_at(i) && key_domain_error<KIND>(key[i], bp);
-    }
-  }
-  auto bucket_at = [&](int i) { return (bk[i / 4] >> (8 * (i & 3))) & 0xFFu; };
-
   // ---- 1. warp-level stable ranking, window by window (Eq.4 terms 1-2) ----
   // Peer masks come from one shared-memory OR of the lane bit per key (the
   // ballot-based voting of Alg.3, in one instruction); masks are
   // double-buffered by window parity, so two __syncwarp per window suffice.
+  // The next window's key is loaded before this window's shared-memory
+  // updates so that its latency overlaps them.
   if constexpr (!SMALLM) {
     for (uint32_t j = lane; j < m; j += 32) {
       mrow0[j] = 0u;
@@ -274,20 +256,31 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
 #pragma unroll
   for (int j = 0; j < NR; ++j) rk[j] = 0u;
   uint32_t c0 = 0, c1 = 0;
+  bool derr = false;
+  uint32_t key_next = valid_at(0) ? in_k[0] : 0u;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = valid_at(i);
+    const uint32_t key = key_next;
+    if (i + 1 < ITEMS) key_next = valid_at(i + 1) ? in_k[32 * (i + 1)] : 0u;
     if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: window past the tail
-    const uint32_t b = bucket_at(i);
+    const uint32_t b = bucket_of<KIND>(key, bp);
+    if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key, bp);
     uint32_t r;
     if constexpr (SMALLM) {
       // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
       const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
-      const uint32_t vm = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
-      const uint32_t zeros = vm & ~ones;
-      r = b ? c1 + __popc(ones & lt) : c0 + __popc(zeros & lt);
-      c1 += __popc(ones);
-      c0 += __popc(zeros);
+      const uint32_t ones_below = __popc(ones & lt);
+      const uint32_t nones = __popc(ones);
+      if (FULL) {
+        r = b ? c1 + ones_below : c0 + lane - ones_below;
+        c0 += 32u - nones;
+      } else {
+        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+        r = b ? c1 + ones_below : c0 + __popc(vm & ~ones & lt);
+        c0 += __popc(vm) - nones;
+      }
+      c1 += nones;
     } else {
       uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
       if (valid) atomicOr(mrow + b, lanebit);
@@ -316,6 +309,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if (WSCAN && a.store_runs && warp == 0) bulk_wait_read();  // previous run stores left s_out
   __syncthreads();
 
+  uint32_t wbase_b[2] = {0u, 0u};  // WSCAN: this warp's slot base of bucket lane + 32k
   if constexpr (WSCAN) {
     // ---- 2'/3'. per-warp scan: this warp's slot base for bucket b is
     //   tile base tb[b] (buckets before b) + counts of b in warps before this one
@@ -362,7 +356,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
           running[k] += tot[k];
         }
         const uint32_t adj = a.store_runs ? 4u * b + ((gs - tb) & 3u) : 0u;
-        mrow0[b] = tb + colp[k] + adj;  // mask row 0 is free after ranking
+        wbase_b[k] = tb + colp[k] + adj;
         if (warp == 0) {
           if (a.store_runs) {
             s_run[b] = tb + adj;
@@ -455,18 +449,27 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if (a.store_runs) __syncthreads();  // shifted bucket bases are visible to the reorder
   }  // block scan
 
-  const uint32_t *brow = WSCAN ? mrow0 : crow;  // this warp's slot base per bucket
+  // this warp's slot base of bucket b (WSCAN: held by lane b mod 32)
+  auto slot_base = [&](uint32_t b) -> uint32_t {
+    if constexpr (WSCAN) {
+      const uint32_t lo = __shfl_sync(0xFFFFFFFFu, wbase_b[0], b & 31u);
+      if (m <= 32) return lo;
+      const uint32_t hi = __shfl_sync(0xFFFFFFFFu, wbase_b[1], b & 31u);
+      return b < 32u ? lo : hi;
+    } else {
+      return crow[b];
+    }
+  };
 
   // ---- 4. reorder into the output buffer (stable local multisplit) -----------
   {
+    uint32_t key[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) key[i] = in_k[32 * i];
     uint32_t slot[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
-      slot[i] = brow[bucket_at(i)] + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
-    if constexpr (!KEEP) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) key[i] = in_k[32 * i];
-    }
+      slot[i] = slot_base(bucket_of<KIND>(key[i], bp)) + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
       if (valid_at(i)) out_k[slot[i]] = key[i];
