@@ -261,15 +261,21 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
+  // the prescan runs two CTAs per range when a range has >= 2 tiles (R then
+  // has <= 2G <= L rows), doubling the loads in flight of the read-only pass
+  const uint32_t kHistSplit = K >= 2 ? 2u : 1u;
+  const uint32_t per = K * lo.T / kHistSplit;
+  const uint32_t gh = (uint32_t)((n + per - 1) / per);
   stage_event(0, s);
-  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, per, gh, H, hdr, s)) != cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
   stage_event(2, s);
   a.mode = kModeRange;
   a.R = H;
   a.tiles_per_cta = K;
-  a.num_ranges = G;
+  a.num_ranges = gh;
+  a.hist_split = kHistSplit;
   const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;

@@ -43,10 +43,10 @@ cudaError_t Launch<KIND>::tile_hist(const uint32_t *keys, uint32_t n, uint32_t t
   return cudaGetLastError();
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, bool BIGM>
+template <int KIND, bool PAIRS, bool SMALLM, bool BIGM, int SCAN>
 static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
   constexpr KfShape sh = kf_shape(PAIRS, BIGM);
-  auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm, !BIGM>;
+  auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm, SCAN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -62,13 +62,16 @@ template <int KIND>
 cudaError_t Launch<KIND>::fused(bool pairs, const KfArgs &a, const BucketParams &bp,
                                 uint32_t grid, cudaStream_t s) {
   if (bp.m <= 2)
-    return pairs ? kf_go<KIND, true, true, false>(a, bp, grid, s)
-                 : kf_go<KIND, false, true, false>(a, bp, grid, s);
+    return pairs ? kf_go<KIND, true, true, false, 1>(a, bp, grid, s)
+                 : kf_go<KIND, false, true, false, 1>(a, bp, grid, s);
+  if (bp.m <= 32)
+    return pairs ? kf_go<KIND, true, false, false, 1>(a, bp, grid, s)
+                 : kf_go<KIND, false, false, false, 1>(a, bp, grid, s);
   if (bp.m <= 64)
-    return pairs ? kf_go<KIND, true, false, false>(a, bp, grid, s)
-                 : kf_go<KIND, false, false, false>(a, bp, grid, s);
-  return pairs ? kf_go<KIND, true, false, true>(a, bp, grid, s)
-               : kf_go<KIND, false, false, true>(a, bp, grid, s);
+    return pairs ? kf_go<KIND, true, false, false, 2>(a, bp, grid, s)
+                 : kf_go<KIND, false, false, false, 2>(a, bp, grid, s);
+  return pairs ? kf_go<KIND, true, false, true, 0>(a, bp, grid, s)
+               : kf_go<KIND, false, false, true, 0>(a, bp, grid, s);
 }
 
 }  // namespace ms

@@ -168,7 +168,8 @@ struct KfArgs {
   uint32_t n;
   uint32_t num_tiles;
   uint32_t tiles_per_cta;
-  uint32_t num_ranges;
+  uint32_t num_ranges;   // rows of R: hist_split rows per CTA range
+  uint32_t hist_split;   // KU CTAs per KF range (more loads in flight in the prescan)
   const uint32_t *R;     // [num_ranges][m]     (kModeRange)
   const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
   const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
@@ -209,11 +210,12 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + 4 * mm * 4;
 }
 
-// WSCAN (m <= 64 shapes): every warp scans the m x W tile counts itself, so a
-// tile needs two CTA barriers (after ranking, after reordering); otherwise a
-// block-wide scan.  running[k] = next global position of bucket lane + 32k
-// (WSCAN) or of bucket tid (block scan).
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, bool WSCAN, bool FULL,
+// SCAN = 1 (m <= 32) / 2 (m <= 64): every warp scans the m x W tile counts
+// itself, holding SCAN buckets per lane, so a tile needs two CTA barriers
+// (after ranking, after reordering); SCAN = 0: block-wide scan.
+// running[k] = next global position of bucket lane + 32k (SCAN > 0) or of
+// bucket tid (block scan).
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int SCAN, bool FULL,
           class OnInputFree>
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
                                            uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
@@ -224,6 +226,8 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   constexpr uint32_t T = NT * ITEMS;
   constexpr int NB = (ITEMS + 3) / 4;  // registers of packed 8-bit buckets
   constexpr int NR = (ITEMS + 1) / 2;  // registers of packed 16-bit ranks
+  constexpr bool WSCAN = SCAN != 0;
+  constexpr int NBL = SCAN == 2 ? 2 : 1;  // buckets per lane in the warp scan
   const uint32_t m = bp.m;
   const uint32_t re = SMALLM ? 2u : m;  // counters per warp row
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -316,7 +320,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     //   (Eq.4 terms 2-3), plus the run padding adj[b] (run stores).
     uint32_t colp[2] = {0u, 0u}, tot[2] = {0u, 0u};
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NBL; ++k) {
       const uint32_t b = lane + 32u * (uint32_t)k;
       if (b < m) {
 #pragma unroll
@@ -331,14 +335,14 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < NBL; ++k) {
         const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl[k], o);
         if (lane >= (uint32_t)o) incl[k] += t;
       }
     }
-    const uint32_t sum0 = __shfl_sync(0xFFFFFFFFu, incl[0], 31);
+    const uint32_t sum0 = NBL == 2 ? __shfl_sync(0xFFFFFFFFu, incl[0], 31) : 0u;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NBL; ++k) {
       const uint32_t b = lane + 32u * (uint32_t)k;
       if (b < m) {
         const uint32_t tb = incl[k] - tot[k] + (k ? sum0 : 0u);
@@ -451,9 +455,10 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
 
   // this warp's slot base of bucket b (WSCAN: held by lane b mod 32)
   auto slot_base = [&](uint32_t b) -> uint32_t {
-    if constexpr (WSCAN) {
+    if constexpr (NBL == 1 && WSCAN) {
+      return __shfl_sync(0xFFFFFFFFu, wbase_b[0], b);
+    } else if constexpr (WSCAN) {
       const uint32_t lo = __shfl_sync(0xFFFFFFFFu, wbase_b[0], b & 31u);
-      if (m <= 32) return lo;
       const uint32_t hi = __shfl_sync(0xFFFFFFFFu, wbase_b[1], b & 31u);
       return b < 32u ? lo : hi;
     } else {
@@ -548,8 +553,9 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   }
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB, bool WSCAN>
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB, int SCAN>
 __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams bp) {
+  constexpr bool WSCAN = SCAN != 0;
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t SW = T * (PAIRS ? 2u : 1u);  // words per stage
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       for (uint32_t r = p; r < a.num_ranges; r += P) {
         const uint32_t v = __ldg(a.R + (size_t)r * m + b);
         tot += v;
-        pre += r < blockIdx.x ? v : 0u;
+        pre += r < blockIdx.x * a.hist_split ? v : 0u;
       }
       s_tot[p * m + b] = tot;
       s_pre[p * m + b] = pre;
@@ -681,11 +687,11 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       }
     };
     if (tn == T)
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, WSCAN, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
                                                       s_cnt, s_delta, s_run, s_wsum, running,
                                                       refill);
     else
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, WSCAN, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
                                                        s_cnt, s_delta, s_run, s_wsum, running,
                                                        refill);
     // no CTA barrier here: the next tile's shared structures are first written
