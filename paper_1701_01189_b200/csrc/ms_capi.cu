@@ -144,13 +144,14 @@ bool overlaps(const void *a, const void *b, uint64_t n) {
 }
 
 cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t per,
-                       uint32_t grid, uint32_t *R, uint32_t *hdr, cudaStream_t s) {
+                       uint32_t grid, uint32_t *R, uint32_t *hdr, unsigned long long *zero,
+                       uint32_t zero_words, cudaStream_t s) {
   switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
+    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
+    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
+    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
+    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
   }
 }
 
@@ -257,25 +258,29 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
     return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
   }
 
-  // level-0 localization: G ranges of K consecutive tiles (2 CTAs per SM)
+  // level-0 localization (Eq.3 with L_0 = G): G ranges of K consecutive tiles,
+  // one CTA each.  KU: range histograms R (m x G); KG: scan of R (and bucket
+  // bases); KF: per range, tiles in order with running per-bucket offsets.
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
-  // the prescan runs two CTAs per range when a range has >= 2 tiles (R then
-  // has <= 2G <= L rows), doubling the loads in flight of the read-only pass
-  const uint32_t kHistSplit = K >= 2 ? 2u : 1u;
-  const uint32_t per = K * lo.T / kHistSplit;
-  const uint32_t gh = (uint32_t)((n + per - 1) / per);
+  const uint32_t C = scan_chunk_tiles(m);
+  const uint32_t nchunks = (G + C - 1) / C;
+  unsigned long long *status = (unsigned long long *)(w + lo.status);
   stage_event(0, s);
-  if (counted(range_hist(pl, keys_in, (uint32_t)n, per, gh, H, hdr, s)) != cudaSuccess)
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, status, nchunks * m, s)) !=
+      cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
+  kg_scan<<<nchunks, kScanThreads, 0, s>>>(H, H, G, m, C, nchunks, status, hdr + 1, base,
+                                           bucket_offsets);
+  if (counted(cudaGetLastError()) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
   a.R = H;
+  a.base = base;
   a.tiles_per_cta = K;
-  a.num_ranges = gh;
-  a.hist_split = kHistSplit;
+  a.num_ranges = G;
   const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;

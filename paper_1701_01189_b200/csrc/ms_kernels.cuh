@@ -112,13 +112,19 @@ __device__ __forceinline__ void hist_flush(uint32_t *cnt, uint32_t m, uint32_t o
 template <int KIND, bool SMALLM>
 __global__ void __launch_bounds__(kThreads)
     ku_range_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t elems_per_cta,
-                  BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+                  BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr,
+                  unsigned long long *__restrict__ zero, uint32_t zero_words) {
   extern __shared__ uint32_t ku_smem[];  // [kWarps][m]
   __shared__ uint32_t s_red[kWarps];
   const uint32_t m = bp.m, tid = threadIdx.x;
   const uint32_t lo = blockIdx.x * elems_per_cta;
   const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + elems_per_cta);
-  if (hdr && blockIdx.x == 0 && tid == 0) hdr[0] = 0u;  // error flag of this call (set by KF)
+  if (hdr && blockIdx.x == 0 && tid < 2) hdr[tid] = 0u;  // [0] error flag (KF), [1] KG ticket
+  if (zero) {  // this CTA's slice of the look-back status words of the KG scan of R
+    const uint32_t per = (zero_words + gridDim.x - 1) / gridDim.x;
+    const uint32_t z0 = blockIdx.x * per, z1 = min(zero_words, z0 + per);
+    for (uint32_t i = z0 + tid; i < z1; i += kThreads) zero[i] = 0ull;
+  }
   if constexpr (!SMALLM) {
     for (uint32_t i = tid; i < kWarps * m; i += kThreads) ku_smem[i] = 0u;
     __syncthreads();
@@ -168,9 +174,8 @@ struct KfArgs {
   uint32_t n;
   uint32_t num_tiles;
   uint32_t tiles_per_cta;
-  uint32_t num_ranges;   // rows of R: hist_split rows per CTA range
-  uint32_t hist_split;   // KU CTAs per KF range (more loads in flight in the prescan)
-  const uint32_t *R;     // [num_ranges][m]     (kModeRange)
+  uint32_t num_ranges;
+  const uint32_t *R;     // [num_ranges][m] column exclusive prefix of the range histograms (kModeRange)
   const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
   const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
   uint32_t *hdr;         // [0] key-domain error flag
@@ -599,68 +604,17 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   issue(t0, 0);
   issue(t0 + 1, 1);
 
-  // ---- level-0 scan (Eq.3 terms 1-2 over the m x G matrix R) -------------------
-  // thread b < m ends with running = sum_{j<b} total_j + sum_{c<blockIdx} R[c][b]
+  // ---- level-0 offsets (Eq.3 terms 1-2): KG has scanned the m x G matrix of
+  // range histograms, R[c][b] = sum_{c'<c} h_{b,c'}, base[b] = sum_{b'<b} total_{b'}
   uint32_t running[2] = {0u, 0u};
   if (a.mode == kModeRange) {
-    uint32_t *s_tot = s_out;  // scratch before the first tile
-    uint32_t *s_pre = s_out + NT;
-    const uint32_t P = NT / m;  // row groups (>= 1)
-    const uint32_t b = tid % m, p = tid / m;
-    if (p < P) {
-      uint32_t tot = 0, pre = 0;
-#pragma unroll 8
-      for (uint32_t r = p; r < a.num_ranges; r += P) {
-        const uint32_t v = __ldg(a.R + (size_t)r * m + b);
-        tot += v;
-        pre += r < blockIdx.x * a.hist_split ? v : 0u;
-      }
-      s_tot[p * m + b] = tot;
-      s_pre[p * m + b] = pre;
-    }
-    __syncthreads();
-    uint32_t t = 0, pr = 0;
-    if (tid < m) {
-      for (uint32_t q = 0; q < P; ++q) {
-        t += s_tot[q * m + tid];
-        pr += s_pre[q * m + tid];
-      }
-    }
-    // exclusive scan of the bucket totals across threads 0..m-1 (block scan)
-    const uint32_t lane = tid & 31, warp = tid >> 5;
-    uint32_t incl = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= (uint32_t)o) incl += x;
-    }
-    if (lane == 31) s_wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t x = lane < (uint32_t)W ? s_wsum[lane] : 0u;
-      uint32_t xi = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
-        if (lane >= (uint32_t)o) xi += y;
-      }
-      if (lane < (uint32_t)W) s_wsum[lane] = xi - x;
-    }
-    __syncthreads();
-    if (tid < m) {
-      const uint32_t gbase = s_wsum[warp] + incl - t;
-      running[0] = gbase + pr;
-      s_delta[tid] = running[0];
-      if (blockIdx.x == 0 && a.bucket_offsets) {
-        a.bucket_offsets[tid] = gbase;
-        if (tid == m - 1) a.bucket_offsets[m] = gbase + t;
-      }
-    }
-    __syncthreads();
     if constexpr (WSCAN) {  // every warp keeps the offsets of buckets lane, lane + 32
       const uint32_t lane_ = tid & 31;
-      running[0] = lane_ < m ? s_delta[lane_] : 0u;
-      running[1] = lane_ + 32 < m ? s_delta[lane_ + 32] : 0u;
+      const uint32_t *row = a.R + (size_t)blockIdx.x * m;
+      if (lane_ < m) running[0] = __ldg(row + lane_) + __ldg(a.base + lane_);
+      if (lane_ + 32 < m) running[1] = __ldg(row + lane_ + 32) + __ldg(a.base + lane_ + 32);
+    } else if (tid < m) {
+      running[0] = __ldg(a.R + (size_t)blockIdx.x * m + tid) + __ldg(a.base + tid);
     }
   }
 

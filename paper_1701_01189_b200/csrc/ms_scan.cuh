@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kScanThreads)
 
   uint32_t sum = 0;
   if (active)
+#pragma unroll 8
     for (uint32_t l = l0; l < l1; ++l) sum += H[(size_t)l * m + j];
   if (active) s_part[g * m + j] = sum;
   __syncthreads();
