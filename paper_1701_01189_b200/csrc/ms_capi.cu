@@ -144,14 +144,17 @@ bool overlaps(const void *a, const void *b, uint64_t n) {
 }
 
 cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t per,
-                       uint32_t grid, uint32_t *R, uint32_t *hdr, unsigned long long *zero,
-                       uint32_t zero_words, cudaStream_t s) {
+                       uint32_t grid, uint32_t *R, uint32_t *hdr, uint32_t *base,
+                       uint32_t *bucket_offsets, cudaStream_t s) {
+  static std::atomic<uint32_t> epochs{1};
+  uint32_t epoch = epochs.fetch_add(1, std::memory_order_relaxed);
+  if (epoch == 0) epoch = epochs.fetch_add(1, std::memory_order_relaxed);
   switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
-    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
-    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
-    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
-    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, zero, zero_words, s);
+    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
+    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
+    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
+    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
+    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
   }
 }
 
@@ -259,22 +262,17 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
 
   // level-0 localization (Eq.3 with L_0 = G): G ranges of K consecutive tiles,
-  // one CTA each.  KU: range histograms R (m x G); KG: scan of R (and bucket
-  // bases); KF: per range, tiles in order with running per-bucket offsets.
+  // one CTA each.  KU: range histograms R (m x G), scanned in place by its last
+  // CTA (with the bucket bases); KF: per range, tiles in order with running
+  // per-bucket offsets.
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
-  const uint32_t C = scan_chunk_tiles(m);
-  const uint32_t nchunks = (G + C - 1) / C;
-  unsigned long long *status = (unsigned long long *)(w + lo.status);
   stage_event(0, s);
-  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, status, nchunks * m, s)) !=
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, base, bucket_offsets, s)) !=
       cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
-  kg_scan<<<nchunks, kScanThreads, 0, s>>>(H, H, G, m, C, nchunks, status, hdr + 1, base,
-                                           bucket_offsets);
-  if (counted(cudaGetLastError()) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
   a.R = H;

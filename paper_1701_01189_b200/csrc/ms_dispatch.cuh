@@ -11,7 +11,8 @@ template <int KIND>
 struct Launch {
   static cudaError_t range_hist(const uint32_t *keys, uint32_t n, uint32_t elems_per_cta,
                                 uint32_t grid, const BucketParams &bp, uint32_t *R, uint32_t *hdr,
-                                unsigned long long *zero, uint32_t zero_words, cudaStream_t s);
+                                uint32_t *base, uint32_t *bucket_offsets, uint32_t epoch,
+                                cudaStream_t s);
   static cudaError_t tile_hist(const uint32_t *keys, uint32_t n, uint32_t tile, uint32_t grid,
                                const BucketParams &bp, uint32_t *H, uint32_t *hdr,
                                cudaStream_t s);
@@ -22,14 +23,14 @@ struct Launch {
 template <int KIND>
 cudaError_t Launch<KIND>::range_hist(const uint32_t *keys, uint32_t n, uint32_t elems_per_cta,
                                      uint32_t grid, const BucketParams &bp, uint32_t *R,
-                                     uint32_t *hdr, unsigned long long *zero, uint32_t zero_words,
-                                     cudaStream_t s) {
+                                     uint32_t *hdr, uint32_t *base, uint32_t *bucket_offsets,
+                                     uint32_t epoch, cudaStream_t s) {
   if (bp.m <= 2)
-    ku_range_hist<KIND, true><<<grid, kThreads, 0, s>>>(keys, n, elems_per_cta, bp, R, hdr, zero,
-                                                         zero_words);
+    ku_range_hist<KIND, true><<<grid, kThreads, 0, s>>>(keys, n, elems_per_cta, bp, R, hdr, base,
+                                                         bucket_offsets, epoch);
   else
     ku_range_hist<KIND, false><<<grid, kThreads, (size_t)kWarps * bp.m * 4u, s>>>(
-        keys, n, elems_per_cta, bp, R, hdr, zero, zero_words);
+        keys, n, elems_per_cta, bp, R, hdr, base, bucket_offsets, epoch);
   return cudaGetLastError();
 }
 

@@ -106,25 +106,107 @@ __device__ __forceinline__ void hist_flush(uint32_t *cnt, uint32_t m, uint32_t o
 }
 
 // ============================================================================
+// Level-0 scan (Eq.3 terms 1-2 with L_0 = G): in place over the G x m matrix R
+// of range histograms, R[c][b] <- sum_{c'<c} R[c'][b]; base[b] <- sum_{b'<b}
+// total_{b'}; bucket_offsets (if any) <- base and n.  One CTA (the last KU CTA
+// to finish): thread (b, p) sums a block of rows of column b.
+// ============================================================================
+__device__ __forceinline__ void level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base,
+                                            uint32_t *bucket_offsets, uint32_t *s_part,
+                                            uint32_t *s_wsum) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t P = kThreads / m, b = tid % m, p = tid / m;
+  const uint32_t S = (G + P - 1) / P;
+  const uint32_t r0 = min(G, p * S), r1 = min(G, r0 + S);
+  uint32_t sum = 0;
+  if (p < P) {
+#pragma unroll 8
+    for (uint32_t r = r0; r < r1; ++r) sum += __ldcg(R + (size_t)r * m + b);
+    s_part[p * m + b] = sum;
+  }
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+  if (p < P) {
+    for (uint32_t q = 0; q < P; ++q) {
+      const uint32_t v = s_part[q * m + b];
+      pre += q < p ? v : 0u;
+      tot += v;
+    }
+  }
+  // exclusive scan over buckets of the totals (threads 0..m-1 hold bucket tid)
+  const uint32_t t = (tid < m) ? tot : 0u;
+  uint32_t incl = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += x;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
+    uint32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+      if (lane >= (uint32_t)o) xi += y;
+    }
+    if (lane < (uint32_t)kWarps) s_wsum[lane] = xi - x;
+  }
+  __syncthreads();
+  if (tid < m) {
+    const uint32_t g = s_wsum[warp] + incl - t;
+    base[tid] = g;
+    if (bucket_offsets) bucket_offsets[tid] = g;
+    if (tid == m - 1) {
+      base[m] = g + t;
+      if (bucket_offsets) bucket_offsets[m] = g + t;
+    }
+  }
+  if (p < P) {
+    uint32_t run = pre;
+    for (uint32_t r = r0; r < r1; ++r) {
+      uint32_t *x = R + (size_t)r * m + b;
+      const uint32_t v = __ldcg(x);
+      *x = run;
+      run += v;
+    }
+  }
+}
+
+// Returns true for the last of `expected` arrivals on an epoch-tagged 64-bit
+// counter {epoch:32 | count:32}: stale values of earlier calls never need a reset.
+__device__ __forceinline__ bool arrive_last(unsigned long long *ctr, uint32_t epoch,
+                                            uint32_t expected) {
+  unsigned long long old = atomicAdd(ctr, 0ull);
+  for (;;) {
+    const unsigned long long nv = ((uint32_t)(old >> 32) == epoch)
+                                      ? old + 1ull
+                                      : (((unsigned long long)epoch << 32) | 1ull);
+    const unsigned long long r = atomicCAS(ctr, old, nv);
+    if (r == old) return (uint32_t)nv == expected;
+    old = r;
+  }
+}
+
+// ============================================================================
 // KU: range histogram (level-0 prescan).  CTA c counts keys
-// [c*E, min(n, (c+1)*E)) where E = K tiles, and writes R[c][0..m).
+// [c*E, min(n, (c+1)*E)) where E = K tiles, and writes R[c][0..m); the last
+// CTA to finish scans R (level0_scan) so that KF reads one row per range.
 // ============================================================================
 template <int KIND, bool SMALLM>
 __global__ void __launch_bounds__(kThreads)
     ku_range_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t elems_per_cta,
-                  BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr,
-                  unsigned long long *__restrict__ zero, uint32_t zero_words) {
+                  BucketParams bp, uint32_t *R, uint32_t *__restrict__ hdr, uint32_t *base,
+                  uint32_t *bucket_offsets, uint32_t epoch) {
   extern __shared__ uint32_t ku_smem[];  // [kWarps][m]
   __shared__ uint32_t s_red[kWarps];
+  __shared__ uint32_t s_part[kThreads];
+  __shared__ uint32_t s_last;
   const uint32_t m = bp.m, tid = threadIdx.x;
   const uint32_t lo = blockIdx.x * elems_per_cta;
   const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + elems_per_cta);
-  if (hdr && blockIdx.x == 0 && tid < 2) hdr[tid] = 0u;  // [0] error flag (KF), [1] KG ticket
-  if (zero) {  // this CTA's slice of the look-back status words of the KG scan of R
-    const uint32_t per = (zero_words + gridDim.x - 1) / gridDim.x;
-    const uint32_t z0 = blockIdx.x * per, z1 = min(zero_words, z0 + per);
-    for (uint32_t i = z0 + tid; i < z1; i += kThreads) zero[i] = 0ull;
-  }
+  if (blockIdx.x == 0 && tid == 0) hdr[0] = 0u;  // key-domain error flag of this call (KF sets it)
   if constexpr (!SMALLM) {
     for (uint32_t i = tid; i < kWarps * m; i += kThreads) ku_smem[i] = 0u;
     __syncthreads();
@@ -132,6 +214,14 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t ones = 0;
   hist_range<KIND, SMALLM>(keys, lo, hi, bp, ku_smem + (tid >> 5) * m, ones);
   hist_flush<SMALLM>(ku_smem, m, ones, hi - lo, R + (size_t)blockIdx.x * m, s_red);
+  __threadfence();  // this CTA's row of R is visible before it is counted
+  __syncthreads();
+  if (tid == 0)
+    s_last = arrive_last(reinterpret_cast<unsigned long long *>(hdr) + 1, epoch, gridDim.x);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  level0_scan(R, gridDim.x, m, base, bucket_offsets, s_part, s_red);
 }
 
 // ============================================================================
