@@ -136,6 +136,20 @@ bool three_launch_mode() {
   return v && !std::strcmp(v, "3pass");
 }
 
+cudaError_t launch_level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base,
+                               uint32_t *bucket_offsets, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kr_level0_scan, R, G, m, base, bucket_offsets);
+}
+
 bool overlaps(const void *a, const void *b, uint64_t n) {
   if (!a || !b || n == 0) return false;
   const char *pa = (const char *)a, *pb = (const char *)b;
@@ -144,17 +158,13 @@ bool overlaps(const void *a, const void *b, uint64_t n) {
 }
 
 cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t per,
-                       uint32_t grid, uint32_t *R, uint32_t *hdr, uint32_t *base,
-                       uint32_t *bucket_offsets, cudaStream_t s) {
-  static std::atomic<uint32_t> epochs{1};
-  uint32_t epoch = epochs.fetch_add(1, std::memory_order_relaxed);
-  if (epoch == 0) epoch = epochs.fetch_add(1, std::memory_order_relaxed);
+                       uint32_t grid, uint32_t *R, uint32_t *hdr, cudaStream_t s) {
   switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
-    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
-    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
-    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
-    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, base, bucket_offsets, epoch, s);
+    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
+    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
   }
 }
 
@@ -262,17 +272,18 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
 
   // level-0 localization (Eq.3 with L_0 = G): G ranges of K consecutive tiles,
-  // one CTA each.  KU: range histograms R (m x G), scanned in place by its last
-  // CTA (with the bucket bases); KF: per range, tiles in order with running
-  // per-bucket offsets.
+  // one CTA each.  KU: range histograms R (m x G); KR: one-CTA scan of R in
+  // place (and the bucket bases); KF: per range, tiles in order with running
+  // per-bucket offsets.  KR and KF are programmatic dependent launches.
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
   stage_event(0, s);
-  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, base, bucket_offsets, s)) !=
-      cudaSuccess)
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
+  if (counted(launch_level0_scan(H, G, m, base, bucket_offsets, s)) != cudaSuccess)
+    return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
   a.R = H;

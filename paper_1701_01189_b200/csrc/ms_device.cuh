@@ -97,6 +97,18 @@ __device__ __forceinline__ uint32_t peer_mask_ballot(uint32_t b, uint32_t active
   return peers;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// griddepcontrol: a kernel launched with programmatic stream serialization may
+// start before its predecessor finishes; griddep_wait() blocks until the
+// predecessor grid has completed and its memory is visible.  Both are no-ops
+// for a normal launch.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- PTX: smem address
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -11,7 +11,6 @@ template <int KIND>
 struct Launch {
   static cudaError_t range_hist(const uint32_t *keys, uint32_t n, uint32_t elems_per_cta,
                                 uint32_t grid, const BucketParams &bp, uint32_t *R, uint32_t *hdr,
-                                uint32_t *base, uint32_t *bucket_offsets, uint32_t epoch,
                                 cudaStream_t s);
   static cudaError_t tile_hist(const uint32_t *keys, uint32_t n, uint32_t tile, uint32_t grid,
                                const BucketParams &bp, uint32_t *H, uint32_t *hdr,
@@ -23,14 +22,12 @@ struct Launch {
 template <int KIND>
 cudaError_t Launch<KIND>::range_hist(const uint32_t *keys, uint32_t n, uint32_t elems_per_cta,
                                      uint32_t grid, const BucketParams &bp, uint32_t *R,
-                                     uint32_t *hdr, uint32_t *base, uint32_t *bucket_offsets,
-                                     uint32_t epoch, cudaStream_t s) {
+                                     uint32_t *hdr, cudaStream_t s) {
   if (bp.m <= 2)
-    ku_range_hist<KIND, true><<<grid, kThreads, 0, s>>>(keys, n, elems_per_cta, bp, R, hdr, base,
-                                                         bucket_offsets, epoch);
+    ku_range_hist<KIND, true><<<grid, kThreads, 0, s>>>(keys, n, elems_per_cta, bp, R, hdr);
   else
     ku_range_hist<KIND, false><<<grid, kThreads, (size_t)kWarps * bp.m * 4u, s>>>(
-        keys, n, elems_per_cta, bp, R, hdr, base, bucket_offsets, epoch);
+        keys, n, elems_per_cta, bp, R, hdr);
   return cudaGetLastError();
 }
 
@@ -57,8 +54,20 @@ static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid,
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<grid, sh.warps * 32, kf_smem_bytes(bp.m, PAIRS), s>>>(a, bp);
-  return cudaGetLastError();
+  // programmatic dependent launch: the prologue (barrier init, TMA of the first
+  // tiles) overlaps the tail of the previous kernel; griddep_wait() orders the rest
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(sh.warps * 32);
+  cfg.dynamicSmemBytes = kf_smem_bytes(bp.m, PAIRS);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // only after our own KR: a user kernel producing the input must complete first
+  cfg.numAttrs = a.mode == kModeRange ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a, bp);
 }
 
 template <int KIND>

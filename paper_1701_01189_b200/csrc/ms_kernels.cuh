@@ -108,8 +108,8 @@ __device__ __forceinline__ void hist_flush(uint32_t *cnt, uint32_t m, uint32_t o
 // ============================================================================
 // Level-0 scan (Eq.3 terms 1-2 with L_0 = G): in place over the G x m matrix R
 // of range histograms, R[c][b] <- sum_{c'<c} R[c'][b]; base[b] <- sum_{b'<b}
-// total_{b'}; bucket_offsets (if any) <- base and n.  One CTA (the last KU CTA
-// to finish): thread (b, p) sums a block of rows of column b.
+// total_{b'}; bucket_offsets (if any) <- base and n.  One CTA: thread (b, p)
+// sums a block of rows of column b.
 // ============================================================================
 __device__ __forceinline__ void level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base,
                                             uint32_t *bucket_offsets, uint32_t *s_part,
@@ -174,35 +174,17 @@ __device__ __forceinline__ void level0_scan(uint32_t *R, uint32_t G, uint32_t m,
   }
 }
 
-// Returns true for the last of `expected` arrivals on an epoch-tagged 64-bit
-// counter {epoch:32 | count:32}: stale values of earlier calls never need a reset.
-__device__ __forceinline__ bool arrive_last(unsigned long long *ctr, uint32_t epoch,
-                                            uint32_t expected) {
-  unsigned long long old = atomicAdd(ctr, 0ull);
-  for (;;) {
-    const unsigned long long nv = ((uint32_t)(old >> 32) == epoch)
-                                      ? old + 1ull
-                                      : (((unsigned long long)epoch << 32) | 1ull);
-    const unsigned long long r = atomicCAS(ctr, old, nv);
-    if (r == old) return (uint32_t)nv == expected;
-    old = r;
-  }
-}
-
 // ============================================================================
 // KU: range histogram (level-0 prescan).  CTA c counts keys
-// [c*E, min(n, (c+1)*E)) where E = K tiles, and writes R[c][0..m); the last
-// CTA to finish scans R (level0_scan) so that KF reads one row per range.
+// [c*E, min(n, (c+1)*E)) where E = K tiles, and writes R[c][0..m).
 // ============================================================================
 template <int KIND, bool SMALLM>
 __global__ void __launch_bounds__(kThreads)
     ku_range_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t elems_per_cta,
-                  BucketParams bp, uint32_t *R, uint32_t *__restrict__ hdr, uint32_t *base,
-                  uint32_t *bucket_offsets, uint32_t epoch) {
+                  BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
   extern __shared__ uint32_t ku_smem[];  // [kWarps][m]
   __shared__ uint32_t s_red[kWarps];
-  __shared__ uint32_t s_part[kThreads];
-  __shared__ uint32_t s_last;
+  griddep_launch_dependents();  // let KR (programmatic launch) get scheduled early
   const uint32_t m = bp.m, tid = threadIdx.x;
   const uint32_t lo = blockIdx.x * elems_per_cta;
   const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + elems_per_cta);
@@ -214,14 +196,16 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t ones = 0;
   hist_range<KIND, SMALLM>(keys, lo, hi, bp, ku_smem + (tid >> 5) * m, ones);
   hist_flush<SMALLM>(ku_smem, m, ones, hi - lo, R + (size_t)blockIdx.x * m, s_red);
-  __threadfence();  // this CTA's row of R is visible before it is counted
-  __syncthreads();
-  if (tid == 0)
-    s_last = arrive_last(reinterpret_cast<unsigned long long *>(hdr) + 1, epoch, gridDim.x);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  level0_scan(R, gridDim.x, m, base, bucket_offsets, s_part, s_red);
+}
+
+// KR: the level-0 scan as one CTA, launched programmatically after KU.
+static __global__ void __launch_bounds__(kThreads)
+    kr_level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base, uint32_t *bucket_offsets) {
+  __shared__ uint32_t s_part[kThreads];
+  __shared__ uint32_t s_red[kWarps];
+  griddep_launch_dependents();  // KF may start its prologue (TMA of its first tiles)
+  griddep_wait();               // KU's range histograms are complete
+  level0_scan(R, G, m, base, bucket_offsets, s_part, s_red);
 }
 
 // ============================================================================
@@ -697,6 +681,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   // ---- level-0 offsets (Eq.3 terms 1-2): KG has scanned the m x G matrix of
   // range histograms, R[c][b] = sum_{c'<c} h_{b,c'}, base[b] = sum_{b'<b} total_{b'}
   uint32_t running[2] = {0u, 0u};
+  griddep_wait();  // programmatic launch: KR's scan (and everything before it) is complete
   if (a.mode == kModeRange) {
     if constexpr (WSCAN) {  // every warp keeps the offsets of buckets lane, lane + 32
       const uint32_t lane_ = tid & 31;
