@@ -61,7 +61,7 @@ Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   lo.L = (uint32_t)((n + lo.T - 1) / lo.T);
   lo.C = scan_chunk_tiles(m);
   lo.nchunks = (lo.L + lo.C - 1) / lo.C;
-  lo.status = lo.H + align_up((size_t)lo.L * m * 4u);
+  lo.status = lo.H + align_up((size_t)lo.L * m * 8u);  // H (or R and its prefixes P)
   lo.total = lo.status + align_up((size_t)lo.nchunks * m * 8u);
   return lo;
 }
@@ -136,10 +136,10 @@ bool three_launch_mode() {
   return v && !std::strcmp(v, "3pass");
 }
 
-cudaError_t launch_level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base,
-                               uint32_t *bucket_offsets, cudaStream_t s) {
+cudaError_t launch_level0_scan(const uint32_t *R, uint32_t *P, uint32_t *Tot, uint32_t G,
+                               uint32_t m, cudaStream_t s) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(1);
+  cfg.gridDim = dim3((m + 31) / 32);
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -147,7 +147,7 @@ cudaError_t launch_level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *ba
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kr_level0_scan, R, G, m, base, bucket_offsets);
+  return cudaLaunchKernelEx(&cfg, kr_level0_scan, R, P, Tot, G, m);
 }
 
 bool overlaps(const void *a, const void *b, uint64_t n) {
@@ -272,9 +272,10 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
 
   // level-0 localization (Eq.3 with L_0 = G): G ranges of K consecutive tiles,
-  // one CTA each.  KU: range histograms R (m x G); KR: one-CTA scan of R in
-  // place (and the bucket bases); KF: per range, tiles in order with running
-  // per-bucket offsets.  KR and KF are programmatic dependent launches.
+  // one CTA each.  KU: range histograms R (m x G); KR: column scan P of R and
+  // the bucket totals; KF: bucket bases from the totals, then per range, tiles
+  // in order with running per-bucket offsets.  KR and KF are programmatic
+  // dependent launches.
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
@@ -282,12 +283,12 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
     return MS_ERR_CUDA;
   stage_event(1, s);
-  if (counted(launch_level0_scan(H, G, m, base, bucket_offsets, s)) != cudaSuccess)
-    return MS_ERR_CUDA;
+  uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
+  if (counted(launch_level0_scan(H, P, base, G, m, s)) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
-  a.R = H;
-  a.base = base;
+  a.R = P;
+  a.Tot = base;
   a.tiles_per_cta = K;
   a.num_ranges = G;
   const cudaError_t e = counted(fused(pl, pairs, a, G, s));

@@ -106,69 +106,45 @@ __device__ __forceinline__ void hist_flush(uint32_t *cnt, uint32_t m, uint32_t o
 }
 
 // ============================================================================
-// Level-0 scan (Eq.3 terms 1-2 with L_0 = G): in place over the G x m matrix R
-// of range histograms, R[c][b] <- sum_{c'<c} R[c'][b]; base[b] <- sum_{b'<b}
-// total_{b'}; bucket_offsets (if any) <- base and n.  One CTA: thread (b, p)
-// sums a block of rows of column b.
+// Level-0 column scan (Eq.3 terms 1-2 with L_0 = G) of the G x m matrix R of
+// range histograms: P[c][b] = sum_{c'<c} R[c'][b] and Tot[b] = sum_c R[c][b].
+// CTA j owns buckets [32j, 32j + 32); thread (b, p) sums a block of rows of
+// column b (P_ row blocks), the blocks are scanned in shared memory, then each
+// thread writes its rows' prefixes.  The bucket bases (exclusive scan of Tot)
+// are formed by every KF CTA from the m totals.
 // ============================================================================
-__device__ __forceinline__ void level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base,
-                                            uint32_t *bucket_offsets, uint32_t *s_part,
-                                            uint32_t *s_wsum) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t P = kThreads / m, b = tid % m, p = tid / m;
-  const uint32_t S = (G + P - 1) / P;
+static __global__ void __launch_bounds__(kThreads)
+    kr_level0_scan(const uint32_t *__restrict__ R, uint32_t *__restrict__ P, uint32_t *__restrict__ Tot,
+                   uint32_t G, uint32_t m) {
+  __shared__ uint32_t s_part[kThreads];
+  griddep_launch_dependents();  // KF may start its prologue (TMA of its first tiles)
+  griddep_wait();               // KU's range histograms are complete
+  const uint32_t tid = threadIdx.x;
+  const uint32_t wb = min(32u, m - blockIdx.x * 32u);  // buckets of this CTA
+  const uint32_t NP = kThreads / wb;                   // row blocks
+  const uint32_t bl = tid % wb, p = tid / wb, b = blockIdx.x * 32u + bl;
+  const uint32_t S = (G + NP - 1) / NP;
   const uint32_t r0 = min(G, p * S), r1 = min(G, r0 + S);
   uint32_t sum = 0;
-  if (p < P) {
+  if (p < NP) {
 #pragma unroll 8
-    for (uint32_t r = r0; r < r1; ++r) sum += __ldcg(R + (size_t)r * m + b);
-    s_part[p * m + b] = sum;
+    for (uint32_t r = r0; r < r1; ++r) sum += __ldg(R + (size_t)r * m + b);
+    s_part[p * wb + bl] = sum;
   }
   __syncthreads();
-  uint32_t pre = 0, tot = 0;
-  if (p < P) {
-    for (uint32_t q = 0; q < P; ++q) {
-      const uint32_t v = s_part[q * m + b];
+  if (p < NP) {
+    uint32_t pre = 0, tot = 0;
+    for (uint32_t q = 0; q < NP; ++q) {
+      const uint32_t v = s_part[q * wb + bl];
       pre += q < p ? v : 0u;
       tot += v;
     }
-  }
-  // exclusive scan over buckets of the totals (threads 0..m-1 hold bucket tid)
-  const uint32_t t = (tid < m) ? tot : 0u;
-  uint32_t incl = t;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= (uint32_t)o) incl += x;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t x = lane < (uint32_t)kWarps ? s_wsum[lane] : 0u;
-    uint32_t xi = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
-      if (lane >= (uint32_t)o) xi += y;
-    }
-    if (lane < (uint32_t)kWarps) s_wsum[lane] = xi - x;
-  }
-  __syncthreads();
-  if (tid < m) {
-    const uint32_t g = s_wsum[warp] + incl - t;
-    base[tid] = g;
-    if (bucket_offsets) bucket_offsets[tid] = g;
-    if (tid == m - 1) {
-      base[m] = g + t;
-      if (bucket_offsets) bucket_offsets[m] = g + t;
-    }
-  }
-  if (p < P) {
+    if (p == 0) Tot[b] = tot;
     uint32_t run = pre;
+#pragma unroll 8
     for (uint32_t r = r0; r < r1; ++r) {
-      uint32_t *x = R + (size_t)r * m + b;
-      const uint32_t v = __ldcg(x);
-      *x = run;
+      const uint32_t v = __ldg(R + (size_t)r * m + b);
+      P[(size_t)r * m + b] = run;
       run += v;
     }
   }
@@ -196,16 +172,6 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t ones = 0;
   hist_range<KIND, SMALLM>(keys, lo, hi, bp, ku_smem + (tid >> 5) * m, ones);
   hist_flush<SMALLM>(ku_smem, m, ones, hi - lo, R + (size_t)blockIdx.x * m, s_red);
-}
-
-// KR: the level-0 scan as one CTA, launched programmatically after KU.
-static __global__ void __launch_bounds__(kThreads)
-    kr_level0_scan(uint32_t *R, uint32_t G, uint32_t m, uint32_t *base, uint32_t *bucket_offsets) {
-  __shared__ uint32_t s_part[kThreads];
-  __shared__ uint32_t s_red[kWarps];
-  griddep_launch_dependents();  // KF may start its prologue (TMA of its first tiles)
-  griddep_wait();               // KU's range histograms are complete
-  level0_scan(R, G, m, base, bucket_offsets, s_part, s_red);
 }
 
 // ============================================================================
@@ -250,6 +216,7 @@ struct KfArgs {
   uint32_t tiles_per_cta;
   uint32_t num_ranges;
   const uint32_t *R;     // [num_ranges][m] column exclusive prefix of the range histograms (kModeRange)
+  const uint32_t *Tot;   // [m] bucket totals (kModeRange)
   const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
   const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
   uint32_t *hdr;         // [0] key-domain error flag
@@ -683,13 +650,42 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t running[2] = {0u, 0u};
   griddep_wait();  // programmatic launch: KR's scan (and everything before it) is complete
   if (a.mode == kModeRange) {
+    // bucket bases = exclusive scan of the totals (block scan; thread b holds bucket b)
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint32_t t = tid < m ? __ldg(a.Tot + tid) : 0u;
+    uint32_t incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += x;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = lane < (uint32_t)W ? s_wsum[lane] : 0u;
+      uint32_t xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+        if (lane >= (uint32_t)o) xi += y;
+      }
+      if (lane < (uint32_t)W) s_wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    if (tid < m) {
+      const uint32_t gbase = s_wsum[warp] + incl - t;
+      s_delta[tid] = gbase + __ldg(a.R + (size_t)blockIdx.x * m + tid);
+      if (blockIdx.x == 0 && a.bucket_offsets) {
+        a.bucket_offsets[tid] = gbase;
+        if (tid == m - 1) a.bucket_offsets[m] = gbase + t;
+      }
+    }
+    __syncthreads();
     if constexpr (WSCAN) {  // every warp keeps the offsets of buckets lane, lane + 32
-      const uint32_t lane_ = tid & 31;
-      const uint32_t *row = a.R + (size_t)blockIdx.x * m;
-      if (lane_ < m) running[0] = __ldg(row + lane_) + __ldg(a.base + lane_);
-      if (lane_ + 32 < m) running[1] = __ldg(row + lane_ + 32) + __ldg(a.base + lane_ + 32);
+      if (lane < m) running[0] = s_delta[lane];
+      if (lane + 32 < m) running[1] = s_delta[lane + 32];
     } else if (tid < m) {
-      running[0] = __ldg(a.R + (size_t)blockIdx.x * m + tid) + __ldg(a.base + tid);
+      running[0] = s_delta[tid];
     }
   }
 
