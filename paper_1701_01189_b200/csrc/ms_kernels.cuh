@@ -125,27 +125,44 @@ static __global__ void __launch_bounds__(kThreads)
   const uint32_t bl = tid % wb, p = tid / wb, b = blockIdx.x * 32u + bl;
   const uint32_t S = (G + NP - 1) / NP;
   const uint32_t r0 = min(G, p * S), r1 = min(G, r0 + S);
+  constexpr uint32_t kMaxS = 32;  // rows held in registers (one batch of loads in flight)
+  uint32_t v[kMaxS];
   uint32_t sum = 0;
   if (p < NP) {
+    if (S <= kMaxS) {
+#pragma unroll
+      for (uint32_t i = 0; i < kMaxS; ++i) v[i] = r0 + i < r1 ? __ldg(R + (size_t)(r0 + i) * m + b) : 0u;
+#pragma unroll
+      for (uint32_t i = 0; i < kMaxS; ++i) sum += v[i];
+    } else {
 #pragma unroll 8
-    for (uint32_t r = r0; r < r1; ++r) sum += __ldg(R + (size_t)r * m + b);
+      for (uint32_t r = r0; r < r1; ++r) sum += __ldg(R + (size_t)r * m + b);
+    }
     s_part[p * wb + bl] = sum;
   }
   __syncthreads();
   if (p < NP) {
     uint32_t pre = 0, tot = 0;
     for (uint32_t q = 0; q < NP; ++q) {
-      const uint32_t v = s_part[q * wb + bl];
-      pre += q < p ? v : 0u;
-      tot += v;
+      const uint32_t x = s_part[q * wb + bl];
+      pre += q < p ? x : 0u;
+      tot += x;
     }
     if (p == 0) Tot[b] = tot;
     uint32_t run = pre;
+    if (S <= kMaxS) {
+#pragma unroll
+      for (uint32_t i = 0; i < kMaxS; ++i) {
+        if (r0 + i < r1) P[(size_t)(r0 + i) * m + b] = run;
+        run += v[i];
+      }
+    } else {
 #pragma unroll 8
-    for (uint32_t r = r0; r < r1; ++r) {
-      const uint32_t v = __ldg(R + (size_t)r * m + b);
-      P[(size_t)r * m + b] = run;
-      run += v;
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t x = __ldg(R + (size_t)r * m + b);
+        P[(size_t)r * m + b] = run;
+        run += x;
+      }
     }
   }
 }
