@@ -272,7 +272,11 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     with ClockSampler(local_rank) as clk:
-        times, stages, launches = time_steps(run, args.steps, args.warmup, flush)
+        # the timed steps carry no stage events (events between kernels would
+        # serialize the programmatic dependent launches); a separate pass below
+        # records the per-stage breakdown for the roofline of the postscan
+        times, _, launches = time_steps(run, args.steps, args.warmup, flush, stage_events=False)
+    _, stages, _ = time_steps(run, max(3, args.steps // 2), 1, flush, stage_events=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -332,7 +336,8 @@ def sweep(args, dev, flush, hbm):
         wl = WORKLOADS[name]
         run = Runner(wl, m, dev)
         steps = 5 if wl["kind"] == "sort" else 10
-        times, stages, _ = time_steps(run, steps, 3, flush)
+        times, _, _ = time_steps(run, steps, 3, flush, stage_events=False)
+        _, stages, _ = time_steps(run, 3, 1, flush, stage_events=True)
         t = sum(times) / len(times)
         rate = wl["n"] / (t * 1e-3) / 1e9
         e = {"value": round(rate, 2), "unit": wl["unit"], "ms": round(t, 4),

@@ -153,6 +153,49 @@ ms_status ms_stage_scan(const uint32_t *H, uint32_t *G, uint64_t L, uint32_t m,
                         uint32_t *bucket_offsets, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Sharded multisplit (Eq.(3) P:408-427 with the GPUs as the first level of
+ * localization, L_0 = G ranks).  Rank s holds input shard s (global elements
+ * N_<s .. N_<s + n_s - 1) and receives output shard s (the same global index
+ * range of the stable multisplit of the rank-order concatenation).  Per rank:
+ *   1. local stable multisplit of the shard (ms_multisplit_*): local bucket
+ *      order, bucket_offsets give the shard's counts C[s][j];
+ *   2. all-gather of the counts C (G x m) over the process group;
+ *   3. ms_shard_plan (host): all-to-all-v counts/displacements and the
+ *      receiver's merge offsets;
+ *   4. all-to-all-v of keys (and values): what rank s sends to rank d is one
+ *      contiguous range of its local order (global positions are monotone in
+ *      it);
+ *   5. ms_shard_merge_* (device): each received element goes to
+ *      merge_offsets[src][f(key)] + its index in the receive buffer.
+ * --------------------------------------------------------------------- */
+
+/* Host only.  C: G*m counts, row s = bucket counts of shard s.  For rank r:
+ * send_counts/displs[d] (elements of r's local order sent to d, as a range),
+ * recv_counts/displs[s] (elements received from s, packed in source order),
+ * merge_offsets[s*m + j] (uint32, modulo 2^32) such that a received element e
+ * (index in the packed receive buffer) from source s with bucket j lands at
+ * output index merge_offsets[s*m + j] + e of rank r's output shard, and
+ * global_bucket_offsets[0..m] (start of each bucket in the global output; may
+ * be NULL).  Returns MS_SUCCESS or MS_ERR_INVALID_VALUE / MS_ERR_UNSUPPORTED
+ * (a rank's shard >= 2^32 elements). */
+ms_status ms_shard_plan(const uint64_t *C, uint32_t G, uint32_t m, uint32_t r,
+                        uint64_t *send_counts, uint64_t *send_displs, uint64_t *recv_counts,
+                        uint64_t *recv_displs, uint32_t *merge_offsets,
+                        uint64_t *global_bucket_offsets);
+
+/* Device merge (step 5): keys_recv/vals_recv (n_recv words, device) are the
+ * packed receive buffers; recv_starts (G+1 uint32, device) the start of each
+ * source's chunk (recv_starts[G] = n_recv); merge_offsets (G*m, device).
+ * Writes keys_out/vals_out (n_recv words, the rank's output shard). */
+ms_status ms_shard_merge_keys(const uint32_t *keys_recv, uint64_t n_recv, const ms_bucket_fn *fn,
+                              const uint32_t *recv_starts, const uint32_t *merge_offsets,
+                              uint32_t G, uint32_t *keys_out, void *stream);
+ms_status ms_shard_merge_pairs(const uint32_t *keys_recv, const uint32_t *vals_recv,
+                               uint64_t n_recv, const ms_bucket_fn *fn,
+                               const uint32_t *recv_starts, const uint32_t *merge_offsets,
+                               uint32_t G, uint32_t *keys_out, uint32_t *vals_out, void *stream);
+
+/* ------------------------------------------------------------------------
  * Instrumentation (host only, thread-local, zero cost when unset).
  * --------------------------------------------------------------------- */
 

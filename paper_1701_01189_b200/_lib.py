@@ -52,6 +52,9 @@ SIGNATURES = [
     ("ms_stage_prescan", _I, [_P, _U64, _FN, _P, _U32, _P]),
     ("ms_stage_scan_workspace_size", _SZ, [_U64, _U32]),
     ("ms_stage_scan", _I, [_P, _P, _U64, _U32, _P, _P, _SZ, _P]),
+    ("ms_shard_plan", _I, [_P, _U32, _U32, _U32, _P, _P, _P, _P, _P, _P]),
+    ("ms_shard_merge_keys", _I, [_P, _U64, _FN, _P, _P, _U32, _P, _P]),
+    ("ms_shard_merge_pairs", _I, [_P, _P, _U64, _FN, _P, _P, _U32, _P, _P, _P]),
     ("ms_set_stage_events", None, [_P]),
     ("ms_launch_count", _U64, []),
 ]

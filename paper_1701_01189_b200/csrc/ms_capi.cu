@@ -3,6 +3,7 @@
 // radix-sort pass driver.  All launches are stream-ordered; nothing here
 // synchronizes except ms_device_status.
 #include <atomic>
+#include <vector>
 #include <cstdlib>
 #include <cstring>
 
@@ -483,6 +484,115 @@ ms_status ms_stage_scan(const uint32_t *H, uint32_t *G, uint64_t L, uint32_t m,
                                            bucket_offsets);
   kg_add_base<<<296, 256, 0, s>>>(G, L * m, m, base);
   return counted(cudaGetLastError(), 3) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+}
+
+ms_status ms_shard_plan(const uint64_t *C, uint32_t G, uint32_t m, uint32_t r,
+                        uint64_t *send_counts, uint64_t *send_displs, uint64_t *recv_counts,
+                        uint64_t *recv_displs, uint32_t *merge_offsets,
+                        uint64_t *global_bucket_offsets) {
+  if (!C || G == 0 || r >= G || m < 1 || m > 256) return MS_ERR_INVALID_VALUE;
+  if (!send_counts || !send_displs || !recv_counts || !recv_displs || !merge_offsets)
+    return MS_ERR_INVALID_VALUE;
+  std::vector<uint64_t> n(G, 0), N0(G + 1, 0), A(m + 1, 0), colpre((size_t)G * m, 0);
+  for (uint32_t s = 0; s < G; ++s) {
+    for (uint32_t j = 0; j < m; ++j) n[s] += C[(size_t)s * m + j];
+    if (n[s] >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
+    N0[s + 1] = N0[s] + n[s];  // output shard s = global [N0[s], N0[s+1])
+  }
+  for (uint32_t j = 0; j < m; ++j) {  // Eq.3 term 1 (A) and term 2 (colpre = B_{j,s})
+    uint64_t run = 0;
+    for (uint32_t s = 0; s < G; ++s) {
+      colpre[(size_t)s * m + j] = run;
+      run += C[(size_t)s * m + j];
+    }
+    A[j + 1] = A[j] + run;
+  }
+  if (global_bucket_offsets)
+    for (uint32_t j = 0; j <= m; ++j) global_bucket_offsets[j] = A[j];
+  // number of shard-s elements whose global position is < x: global position is
+  // monotone along s's local (bucket-major) order, so this is a prefix of it
+  auto below = [&](uint32_t s, uint64_t x) {
+    uint64_t cnt = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint64_t g = A[j] + colpre[(size_t)s * m + j], c = C[(size_t)s * m + j];
+      cnt += x <= g ? 0 : (x - g < c ? x - g : c);
+    }
+    return cnt;
+  };
+  for (uint32_t d = 0; d < G; ++d) {  // what r sends to d: one range of r's local order
+    const uint64_t lo = below(r, N0[d]), hi = below(r, N0[d + 1]);
+    send_displs[d] = lo;
+    send_counts[d] = hi - lo;
+  }
+  uint64_t packed = 0;
+  for (uint32_t s = 0; s < G; ++s) {  // what r receives from s, packed in source order
+    const uint64_t lo = below(s, N0[r]), hi = below(s, N0[r + 1]);
+    recv_counts[s] = hi - lo;
+    recv_displs[s] = packed;
+    // element e of the receive buffer from s is s's local index q = lo + (e - packed);
+    // bucket j: global = A_j + B_{j,s} + (q - localbase_{s,j}); output index = global - N0[r]
+    uint64_t lb = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint64_t g = A[j] + colpre[(size_t)s * m + j];
+      merge_offsets[(size_t)s * m + j] = (uint32_t)(g - lb + lo - N0[r] - packed);
+      lb += C[(size_t)s * m + j];
+    }
+    packed += hi - lo;
+  }
+  return MS_SUCCESS;
+}
+
+static ms_status shard_merge(const uint32_t *keys_recv, const uint32_t *vals_recv, uint64_t n_recv,
+                             const ms_bucket_fn *fn, const uint32_t *recv_starts,
+                             const uint32_t *merge_offsets, uint32_t G, uint32_t *keys_out,
+                             uint32_t *vals_out, void *stream, bool pairs) {
+  ms_status st = validate_fn(fn);
+  if (st != MS_SUCCESS) return st;
+  if (n_recv >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
+  if (n_recv == 0) return MS_SUCCESS;
+  if (!keys_recv || !keys_out || !recv_starts || !merge_offsets || G == 0 ||
+      (pairs && (!vals_recv || !vals_out)))
+    return MS_ERR_INVALID_VALUE;
+  const Plan pl = make_plan(fn);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (pl.kind) {
+    case kIdentity:
+      e = Launch<kIdentity>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
+                                   recv_starts, merge_offsets, G, keys_out, vals_out, s);
+      break;
+    case kDelta:
+      e = Launch<kDelta>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp, recv_starts,
+                                merge_offsets, G, keys_out, vals_out, s);
+      break;
+    case kRadix:
+      e = Launch<kRadix>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp, recv_starts,
+                                merge_offsets, G, keys_out, vals_out, s);
+      break;
+    case kTopBits:
+      e = Launch<kTopBits>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
+                                  recv_starts, merge_offsets, G, keys_out, vals_out, s);
+      break;
+    default:
+      e = Launch<kDeltaShift>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
+                                     recv_starts, merge_offsets, G, keys_out, vals_out, s);
+  }
+  return counted(e) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+}
+
+ms_status ms_shard_merge_keys(const uint32_t *keys_recv, uint64_t n_recv, const ms_bucket_fn *fn,
+                              const uint32_t *recv_starts, const uint32_t *merge_offsets,
+                              uint32_t G, uint32_t *keys_out, void *stream) {
+  return shard_merge(keys_recv, nullptr, n_recv, fn, recv_starts, merge_offsets, G, keys_out,
+                     nullptr, stream, false);
+}
+
+ms_status ms_shard_merge_pairs(const uint32_t *keys_recv, const uint32_t *vals_recv,
+                               uint64_t n_recv, const ms_bucket_fn *fn,
+                               const uint32_t *recv_starts, const uint32_t *merge_offsets,
+                               uint32_t G, uint32_t *keys_out, uint32_t *vals_out, void *stream) {
+  return shard_merge(keys_recv, vals_recv, n_recv, fn, recv_starts, merge_offsets, G, keys_out,
+                     vals_out, stream, true);
 }
 
 void ms_set_stage_events(void *const *events) { g_stage_events = events; }

@@ -17,7 +17,25 @@ struct Launch {
                                cudaStream_t s);
   static cudaError_t fused(bool pairs, const KfArgs &a, const BucketParams &bp, uint32_t grid,
                            cudaStream_t s);
+  static cudaError_t merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
+                           const BucketParams &bp, const uint32_t *starts, const uint32_t *offs,
+                           uint32_t G, uint32_t *keys_out, uint32_t *vals_out, cudaStream_t s);
 };
+
+template <int KIND>
+cudaError_t Launch<KIND>::merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
+                                const BucketParams &bp, const uint32_t *starts,
+                                const uint32_t *offs, uint32_t G, uint32_t *keys_out,
+                                uint32_t *vals_out, cudaStream_t s) {
+  const uint32_t grid = min((n + 255u) / 256u, 148u * 16u);
+  if (pairs)
+    kx_shard_merge<KIND, true><<<grid, 256, 0, s>>>(keys, vals, n, bp, starts, offs, G, keys_out,
+                                                    vals_out);
+  else
+    kx_shard_merge<KIND, false><<<grid, 256, 0, s>>>(keys, vals, n, bp, starts, offs, G, keys_out,
+                                                     vals_out);
+  return cudaGetLastError();
+}
 
 template <int KIND>
 cudaError_t Launch<KIND>::range_hist(const uint32_t *keys, uint32_t n, uint32_t elems_per_cta,

@@ -742,4 +742,26 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   if (a.store_runs) bulk_wait_all();  // run stores complete before smem is released
 }
 
+// ============================================================================
+// KX: receiver merge of the sharded multisplit.  Element e of the packed
+// receive buffer comes from source s (recv_starts[s] <= e < recv_starts[s+1])
+// and goes to out[merge_offsets[s][f(key)] + e].  Runs of one (source, bucket)
+// are consecutive in e, so stores are coalesced within each run.
+// ============================================================================
+template <int KIND, bool PAIRS>
+__global__ void __launch_bounds__(256)
+    kx_shard_merge(const uint32_t *__restrict__ keys, const uint32_t *__restrict__ vals,
+                   uint32_t n, BucketParams bp, const uint32_t *__restrict__ starts,
+                   const uint32_t *__restrict__ offs, uint32_t G, uint32_t *__restrict__ keys_out,
+                   uint32_t *__restrict__ vals_out) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    uint32_t s = 0;
+    while (s + 1 < G && __ldg(starts + s + 1) <= e) ++s;
+    const uint32_t k = keys[e];
+    const uint32_t p = __ldg(offs + (size_t)s * bp.m + bucket_of<KIND>(k, bp)) + e;
+    keys_out[p] = k;
+    if constexpr (PAIRS) vals_out[p] = vals[e];
+  }
+}
+
 }  // namespace ms
