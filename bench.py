@@ -44,6 +44,9 @@ WORKLOADS = {
                         desc="key-value multisplit, n=2^27, identity buckets (configs[2])"),
     "ms_pairs_c3_skew": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
                              dist="skew", desc="key-value multisplit, n=2^27, identity, 90% one bucket (configs[2])"),
+    "ms_sharded_c5": dict(n=1 << 30, pairs=True, kind="delta", m=256, unit="Gpairs/s", bpe=20,
+                          desc="sharded key-value multisplit, n=2^30 pairs in total over the ranks, m=256 "
+                               "delta buckets (configs[4]); n is per job, split evenly", strong=True),
     "sort_keys": dict(n=1 << 28, pairs=False, kind="sort", m=256, unit="Gkeys/s", bpe=48,
                       desc="multisplit LSD radix sort, 2^28 uint32 keys, 4 x 8-bit (configs[3])"),
     "sort_pairs": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80,
@@ -125,14 +128,17 @@ class ClockSampler:
 class Runner:
     """Holds device inputs/outputs for one workload and runs one step per call."""
 
-    def __init__(self, wl: dict, m: int, dev, rank: int = 0):
+    def __init__(self, wl: dict, m: int, dev, rank: int = 0, world: int = 1):
         import torch
         import paper_1701_01189_b200 as ms
         from gen import device as gdev
         from gen import inputs as gen
 
         self.torch, self.ms, self.wl, self.m = torch, ms, wl, m
-        n = wl["n"]
+        self.world = world
+        # N > 1: the sharded multisplit (all-gather of counts + all-to-all-v over
+        # NCCL); weak scaling (n per rank) unless the workload fixes the job size
+        n = wl["n"] // world if wl.get("strong") else wl["n"]
         self.n = n
         kind = wl["kind"]
         dist = {"skew": gen.DIST_SKEW, "binomial": gen.DIST_BINOMIAL}.get(wl.get("dist"), gen.DIST_UNIFORM)
@@ -165,6 +171,10 @@ class Runner:
     def step(self, keys=None, ko=None):
         keys = self.keys if keys is None else keys
         ko = self.ko if ko is None else ko
+        if self.world > 1:
+            from paper_1701_01189_b200 import sharded
+            self.ko, self.vo, _ = sharded.sharded_multisplit(keys, self.vals, self.bucket)
+            return
         if self.bucket is None:
             self.ms.radix_sort(keys, self.vals, out_keys=ko, out_values=self.vo, workspace=self.ws)
         else:
@@ -267,7 +277,9 @@ def run_ours(args, rank, world, local_rank):
     from gen import device as gdev
     flush = lambda: gdev.flush_(scratch)  # noqa: E731
 
-    run = Runner(wl, m, dev, rank)
+    if world > 1 and wl["kind"] == "sort":
+        raise SystemExit("the sort workloads run on one GPU")
+    run = Runner(wl, m, dev, rank, world)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -276,7 +288,9 @@ def run_ours(args, rank, world, local_rank):
         # serialize the programmatic dependent launches); a separate pass below
         # records the per-stage breakdown for the roofline of the postscan
         times, _, launches = time_steps(run, args.steps, args.warmup, flush, stage_events=False)
-    _, stages, _ = time_steps(run, max(3, args.steps // 2), 1, flush, stage_events=True)
+    stages = None
+    if world == 1:
+        _, stages, _ = time_steps(run, max(3, args.steps // 2), 1, flush, stage_events=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -286,7 +300,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     n = run.n
-    value = n * world / (ms_step * 1e-3) / 1e9
+    value = n * world / (ms_step * 1e-3) / 1e9  # all ranks' elements / max-over-ranks step time
     # dominant kernel = postscan (KS); algorithmic bytes per launch: read + write of keys (+ values)
     roofline = None
     if stages is not None:
@@ -304,10 +318,11 @@ def run_ours(args, rank, world, local_rank):
         else f"radix sort {wl['unit']} ({args.workload})",
         "value": round(value, 3), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded counter-based generator)",
-        "config": {"workload": wl["desc"], "n": n, "m": m, "bucket": wl["kind"],
+        "scaling": "strong" if wl.get("strong") else "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded counter-based generator)",
+        "config": {"workload": wl["desc"], "n_per_rank": n, "n_total": n * world, "m": m, "bucket": wl["kind"],
                    "pairs": wl["pairs"], "l2": "flushed before every timed step (512 MiB write)",
-                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+                   "parallelism": f"sharded{world} (NCCL all-gather + all-to-all-v)" if world > 1 else "single"},
         "hbm_roofline_frac_whole_op": round(whole_frac, 4),
         "roofline": roofline,
         "e2e": {"value": round(n * world / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl["unit"],
