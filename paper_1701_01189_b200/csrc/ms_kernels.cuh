@@ -264,13 +264,15 @@ __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
   return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;  // m > 64 never uses run stores
 }
 // Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
-// | per-warp counts [W][m] | delta[m] | run table [3][m]
+// | per-warp counts [W][m] | per-warp running slots [W][m] | delta[m] | run table [3][m]
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   const bool bigm = m > 64;
   const size_t T = kf_tile(pairs, bigm), W = (size_t)kf_shape(pairs, bigm).warps;
   const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + 3 * W * mm * 4 + 4 * mm * 4;
+  const size_t rows = bigm ? 3 : 4;  // the per-warp running-slot rows exist for m <= 64 only
+  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 +
+         4 * mm * 4;
 }
 
 // SCAN = 1 (m <= 32) / 2 (m <= 64): every warp scans the m x W tile counts
@@ -283,12 +285,11 @@ template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int SCAN, bool FU
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
                                            uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
                                            uint32_t OS, uint32_t *s_mask, uint32_t *s_cnt,
-                                           uint32_t *s_delta, uint32_t *s_run, uint32_t *s_wsum,
-                                           uint32_t (&running)[2], OnInputFree on_input_free) {
+                                           uint32_t *s_base, uint32_t *s_delta, uint32_t *s_run,
+                                           uint32_t *s_wsum, uint32_t (&running)[2],
+                                           OnInputFree on_input_free) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
-  constexpr int NB = (ITEMS + 3) / 4;  // registers of packed 8-bit buckets
-  constexpr int NR = (ITEMS + 1) / 2;  // registers of packed 16-bit ranks
   constexpr bool WSCAN = SCAN != 0;
   constexpr int NBL = SCAN == 2 ? 2 : 1;  // buckets per lane in the warp scan
   const uint32_t m = bp.m;
@@ -305,69 +306,41 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   uint32_t *out_v = s_out + OS;
   auto valid_at = [&](int i) { return FULL || wbase + (uint32_t)i * 32u + lane < tn; };
 
-  // ---- 1. warp-level stable ranking, window by window (Eq.4 terms 1-2) ----
-  // Peer masks come from one shared-memory OR of the lane bit per key (the
-  // ballot-based voting of Alg.3, P:909-930, in one instruction); masks are
-  // double-buffered by window parity, so two __syncwarp per window suffice.
-  // The next window's key is loaded before this window's shared-memory
-  // updates so that its latency overlaps them.
+  // ---- 1. count pass: each warp's bucket counts (Eq.4 terms 2-3 need them
+  //         before any element can be placed) -----------------------------------
   if constexpr (!SMALLM) {
     for (uint32_t j = lane; j < m; j += 32) {
       mrow0[j] = 0u;
       mrow1[j] = 0u;
       crow[j] = 0u;
     }
+    __syncwarp();
   }
-  __syncwarp();
-  uint32_t rk[NR];  // rank within the warp (< 32 ITEMS), two 16-bit ranks per register
-#pragma unroll
-  for (int j = 0; j < NR; ++j) rk[j] = 0u;
-  uint32_t c0 = 0, c1 = 0;
   bool derr = false;
-  uint32_t key_next = valid_at(0) ? in_k[0] : 0u;
+  {
+    uint32_t key[ITEMS];
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const bool valid = valid_at(i);
-    const uint32_t key = key_next;
-    if (i + 1 < ITEMS) key_next = valid_at(i + 1) ? in_k[32 * (i + 1)] : 0u;
-    if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: window past the tail
-    const uint32_t b = bucket_of<KIND>(key, bp);
-    if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key, bp);
-    uint32_t r;
-    if constexpr (SMALLM) {
-      // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
-      const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
-      const uint32_t ones_below = __popc(ones & lt);
-      const uint32_t nones = __popc(ones);
-      if (FULL) {
-        r = b ? c1 + ones_below : c0 + lane - ones_below;
-        c0 += 32u - nones;
+    for (int i = 0; i < ITEMS; ++i) key[i] = valid_at(i) ? in_k[32 * i] : 0u;
+    uint32_t c0 = 0, c1 = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = valid_at(i);
+      const uint32_t b = bucket_of<KIND>(key[i], bp);
+      if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+      if constexpr (SMALLM) {
+        const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
+        const uint32_t vm = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
+        c1 += __popc(ones);
+        c0 += __popc(vm & ~ones);
       } else {
-        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
-        r = b ? c1 + ones_below : c0 + __popc(vm & ~ones & lt);
-        c0 += __popc(vm) - nones;
-      }
-      c1 += nones;
-    } else {
-      uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
-      if (valid) atomicOr(mrow + b, lanebit);
-      __syncwarp();
-      const uint32_t peers = valid ? mrow[b] : 0u;
-      const uint32_t cnt = valid ? crow[b] : 0u;
-      const uint32_t below = peers & lt;
-      r = cnt + __popc(below);
-      __syncwarp();                // every lane has read before the leader writes
-      if (valid && below == 0u) {  // group leader: clear this parity's mask, advance the count
-        mrow[b] = 0u;
-        crow[b] = cnt + __popc(peers);
+        if (valid) atomicAdd(crow + b, 1u);
       }
     }
-    rk[i / 2] |= r << (16 * (i & 1));
-  }
-  if constexpr (SMALLM) {
-    if (lane == 0) {
-      crow[0] = c0;
-      crow[1] = c1;
+    if constexpr (SMALLM) {
+      if (lane == 0) {
+        crow[0] = c0;
+        crow[1] = c1;
+      }
     }
   }
   if constexpr (KIND == kIdentity) {
@@ -376,10 +349,10 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if (WSCAN && a.store_runs && warp == 0) bulk_wait_read();  // previous run stores left s_out
   __syncthreads();
 
-  uint32_t wbase_b[2] = {0u, 0u};  // WSCAN: this warp's slot base of bucket lane + 32k
+  uint32_t *brow = WSCAN ? s_base + warp * re : crow;  // this warp's running slot per bucket
   if constexpr (WSCAN) {
-    // ---- 2'/3'. per-warp scan: this warp's slot base for bucket b is
-    //   tile base tb[b] (buckets before b) + counts of b in warps before this one
+    // ---- 2'. per-warp scan: this warp's first slot for bucket b is the tile
+    //   base tb[b] (buckets before b) + counts of b in warps before this one
     //   (Eq.4 terms 2-3), plus the run padding adj[b] (run stores).
     uint32_t colp[2] = {0u, 0u}, tot[2] = {0u, 0u};
 #pragma unroll
@@ -423,7 +396,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
           running[k] += tot[k];
         }
         const uint32_t adj = a.store_runs ? 4u * b + ((gs - tb) & 3u) : 0u;
-        wbase_b[k] = tb + colp[k] + adj;
+        brow[b] = tb + colp[k] + adj;
         if (warp == 0) {
           if (a.store_runs) {
             s_run[b] = tb + adj;
@@ -513,40 +486,62 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       s_delta[tid] = gs - tb;
     }
   }
-  if (a.store_runs) __syncthreads();  // shifted bucket bases are visible to the reorder
+  __syncthreads();  // bucket threads have read warp 0's bases before it starts placing
   }  // block scan
 
-  // this warp's slot base of bucket b (WSCAN: held by lane b mod 32)
-  auto slot_base = [&](uint32_t b) -> uint32_t {
-    if constexpr (NBL == 1 && WSCAN) {
-      return __shfl_sync(0xFFFFFFFFu, wbase_b[0], b);
-    } else if constexpr (WSCAN) {
-      const uint32_t lo = __shfl_sync(0xFFFFFFFFu, wbase_b[0], b & 31u);
-      const uint32_t hi = __shfl_sync(0xFFFFFFFFu, wbase_b[1], b & 31u);
-      return b < 32u ? lo : hi;
-    } else {
-      return crow[b];
-    }
-  };
 
-  // ---- 4. reorder into the output buffer (stable local multisplit) -----------
+  // ---- 3. rank and place, window by window (Eq.4 term 1 + the running slot) --
+  // Peer masks come from one shared-memory OR of the lane bit per key (the
+  // ballot-based voting of Alg.3, P:909-930, in one instruction); masks are
+  // double-buffered by window parity.  slot = this warp's running slot of the
+  // bucket + same-bucket lanes below; the key (and value) is stored there.
   {
-    uint32_t key[ITEMS];
+    uint32_t base0 = 0, base1 = 0, c0 = 0, c1 = 0;
+    if constexpr (SMALLM) {
+      base0 = brow[0];
+      base1 = brow[1];
+    }
+    uint32_t key_next = valid_at(0) ? in_k[0] : 0u;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) key[i] = in_k[32 * i];
-    uint32_t slot[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      slot[i] = slot_base(bucket_of<KIND>(key[i], bp)) + ((rk[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      if (valid_at(i)) out_k[slot[i]] = key[i];
-    if constexpr (PAIRS) {
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) key[i] = in_v[32 * i];
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i)
-        if (valid_at(i)) out_v[slot[i]] = key[i];
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = valid_at(i);
+      const uint32_t key = key_next;
+      if (i + 1 < ITEMS) key_next = valid_at(i + 1) ? in_k[32 * (i + 1)] : 0u;
+      if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: past the tail
+      const uint32_t b = bucket_of<KIND>(key, bp);
+      uint32_t slot;
+      if constexpr (SMALLM) {
+        // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
+        const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
+        const uint32_t ones_below = __popc(ones & lt);
+        const uint32_t nones = __popc(ones);
+        if (FULL) {
+          slot = b ? base1 + c1 + ones_below : base0 + c0 + lane - ones_below;
+          c0 += 32u - nones;
+        } else {
+          const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+          slot = b ? base1 + c1 + ones_below : base0 + c0 + __popc(vm & ~ones & lt);
+          c0 += __popc(vm) - nones;
+        }
+        c1 += nones;
+      } else {
+        uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
+        if (valid) atomicOr(mrow + b, lanebit);
+        __syncwarp();
+        const uint32_t peers = valid ? mrow[b] : 0u;
+        const uint32_t first = valid ? brow[b] : 0u;
+        const uint32_t below = peers & lt;
+        slot = first + __popc(below);
+        __syncwarp();                // every lane has read before the leader writes
+        if (valid && below == 0u) {  // group leader: clear this parity's mask, advance the slot
+          mrow[b] = 0u;
+          brow[b] = first + __popc(peers);
+        }
+      }
+      if (valid) {
+        out_k[slot] = key;
+        if constexpr (PAIRS) out_v[slot] = in_v[32 * i];
+      }
     }
   }
   __syncthreads();
@@ -632,7 +627,8 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t *s_out = stage0 + 2 * SW;
   uint32_t *s_mask = s_out + OS * (PAIRS ? 2u : 1u);
   uint32_t *s_cnt = s_mask + 2 * W * mm;
-  uint32_t *s_delta = s_cnt + W * mm;
+  uint32_t *s_base = s_cnt + W * mm;  // WSCAN only
+  uint32_t *s_delta = WSCAN ? s_base + W * mm : s_base;
   uint32_t *s_run = s_delta + mm;
   const uint32_t tid = threadIdx.x;
   constexpr uint32_t kProducer = NT - 32;  // lane 0 of the last warp issues the TMA loads
@@ -730,12 +726,12 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     };
     if (tn == T)
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                      s_cnt, s_delta, s_run, s_wsum, running,
-                                                      refill);
+                                                      s_cnt, s_base, s_delta, s_run, s_wsum,
+                                                      running, refill);
     else
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                       s_cnt, s_delta, s_run, s_wsum, running,
-                                                       refill);
+                                                       s_cnt, s_base, s_delta, s_run, s_wsum,
+                                                       running, refill);
     // no CTA barrier here: the next tile's shared structures are first written
     // after barriers that every thread reaches only once done with this tile
   }
