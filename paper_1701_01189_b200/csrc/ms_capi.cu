@@ -39,8 +39,10 @@ uint32_t scan_chunk_tiles(uint32_t m) {
   return c < 1 ? 1 : c;
 }
 
-uint32_t tile_elems(uint32_t m, bool pairs) { return kf_tile(pairs, m > 64); }
-uint32_t ctas_per_sm(uint32_t m, bool pairs) { return (uint32_t)kf_shape(pairs, m > 64).ctas_per_sm; }
+uint32_t tile_elems(uint32_t m, bool pairs) { return kf_tile(pairs, kf_class(m)); }
+uint32_t ctas_per_sm(uint32_t m, bool pairs) {
+  return (uint32_t)kf_shape(pairs, kf_class(m)).ctas_per_sm;
+}
 
 // Workspace: [hdr 256 B][base 1280 B][R or H: L*m words][KG status: nchunks*m u64]
 // (the level-0 histogram R needs G <= L rows; the three-launch mode needs L rows of H).

@@ -61,14 +61,14 @@ cudaError_t Launch<KIND>::tile_hist(const uint32_t *keys, uint32_t n, uint32_t t
   return cudaGetLastError();
 }
 
-template <int KIND, bool PAIRS, bool SMALLM, bool BIGM, int SCAN>
+template <int KIND, bool PAIRS, bool SMALLM, int CLS, int SCAN>
 static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
-  constexpr KfShape sh = kf_shape(PAIRS, BIGM);
+  constexpr KfShape sh = kf_shape(PAIRS, CLS);
   auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm, SCAN>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kf_smem_bytes(BIGM ? kMaxBuckets : 64, PAIRS));
+                                         (int)kf_smem_bytes(CLS == 0 ? 32 : (CLS == 1 ? 64 : kMaxBuckets), PAIRS));
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -92,16 +92,16 @@ template <int KIND>
 cudaError_t Launch<KIND>::fused(bool pairs, const KfArgs &a, const BucketParams &bp,
                                 uint32_t grid, cudaStream_t s) {
   if (bp.m <= 2)
-    return pairs ? kf_go<KIND, true, true, false, 1>(a, bp, grid, s)
-                 : kf_go<KIND, false, true, false, 1>(a, bp, grid, s);
+    return pairs ? kf_go<KIND, true, true, 0, 1>(a, bp, grid, s)
+                 : kf_go<KIND, false, true, 0, 1>(a, bp, grid, s);
   if (bp.m <= 32)
-    return pairs ? kf_go<KIND, true, false, false, 1>(a, bp, grid, s)
-                 : kf_go<KIND, false, false, false, 1>(a, bp, grid, s);
+    return pairs ? kf_go<KIND, true, false, 0, 1>(a, bp, grid, s)
+                 : kf_go<KIND, false, false, 0, 1>(a, bp, grid, s);
   if (bp.m <= 64)
-    return pairs ? kf_go<KIND, true, false, false, 2>(a, bp, grid, s)
-                 : kf_go<KIND, false, false, false, 2>(a, bp, grid, s);
-  return pairs ? kf_go<KIND, true, false, true, 0>(a, bp, grid, s)
-               : kf_go<KIND, false, false, true, 0>(a, bp, grid, s);
+    return pairs ? kf_go<KIND, true, false, 1, 2>(a, bp, grid, s)
+                 : kf_go<KIND, false, false, 1, 2>(a, bp, grid, s);
+  return pairs ? kf_go<KIND, true, false, 2, 0>(a, bp, grid, s)
+               : kf_go<KIND, false, false, 2, 0>(a, bp, grid, s);
 }
 
 }  // namespace ms

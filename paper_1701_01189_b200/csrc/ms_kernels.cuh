@@ -243,36 +243,40 @@ struct KfArgs {
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
 };
 
-// CTA shapes (warps W, windows per warp ITEMS; tile T = 32 W ITEMS):
-//   keys, m <= 64 : 16 x 16 (T 8192)    pairs, m <= 64 : 16 x 8 (T 4096)
-//   keys, m >  64 :  8 x 16 (T 4096)    pairs, m >  64 :  8 x 8 (T 2048)
-// chosen so that two (m <= 64) or three (m > 64) CTAs fit in an SM's 228 KB.
+// CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),
+// chosen so that two (m <= 32) or three (m > 32) CTAs fit in an SM's 228 KB:
+//   class 0, m <= 32 : keys 16 x 16 (T 8192), pairs 16 x 8 (T 4096), warp scan, 1 bucket/lane
+//   class 1, m <= 64 : keys  8 x 16 (T 4096), pairs  8 x 8 (T 2048), warp scan, 2 buckets/lane
+//   class 2, m >  64 : keys  8 x 16 (T 4096), pairs  8 x 8 (T 2048), block scan
+__host__ __device__ constexpr int kf_class(uint32_t m) { return m <= 32 ? 0 : (m <= 64 ? 1 : 2); }
 struct KfShape {
   int warps, items, ctas_per_sm;
 };
-__host__ __device__ constexpr KfShape kf_shape(bool pairs, bool bigm) {
-  return bigm ? KfShape{8, pairs ? 8 : 16, 3} : KfShape{16, pairs ? 8 : 16, 2};
+__host__ __device__ constexpr KfShape kf_shape(bool pairs, int cls) {
+  return cls == 0 ? KfShape{16, pairs ? 8 : 16, 2} : KfShape{8, pairs ? 8 : 16, 3};
 }
-__host__ __device__ constexpr uint32_t kf_tile(bool pairs, bool bigm) {
-  return 32u * (uint32_t)kf_shape(pairs, bigm).warps * (uint32_t)kf_shape(pairs, bigm).items;
+__host__ __device__ constexpr uint32_t kf_tile(bool pairs, int cls) {
+  return 32u * (uint32_t)kf_shape(pairs, cls).warps * (uint32_t)kf_shape(pairs, cls).items;
 }
 
 // Reordered-tile capacity: T slots plus up to 4m+4 of padding, so that every
 // bucket run can start at the same offset mod 4 as its global destination
-// (16-byte aligned TMA bulk stores of the run body).
+// (16-byte aligned TMA bulk stores of the run body; m <= 64 only).
 __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
-  return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;  // m > 64 never uses run stores
+  return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;
 }
 // Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
-// | per-warp counts [W][m] | per-warp running slots [W][m] | delta[m] | run table [3][m]
+// | per-warp counts [W][m] | per-warp running slots [W][m] (m <= 64) | delta[m]
+// | run table [3][m] (m <= 64)
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
-  const bool bigm = m > 64;
-  const size_t T = kf_tile(pairs, bigm), W = (size_t)kf_shape(pairs, bigm).warps;
+  const int cls = kf_class(m);
+  const size_t T = kf_tile(pairs, cls), W = (size_t)kf_shape(pairs, cls).warps;
   const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  const size_t rows = bigm ? 3 : 4;  // the per-warp running-slot rows exist for m <= 64 only
+  const size_t rows = cls == 2 ? 3 : 4;
+  const size_t tables = cls == 2 ? 1 : 4;
   return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 +
-         4 * mm * 4;
+         tables * mm * 4;
 }
 
 // SCAN = 1 (m <= 32) / 2 (m <= 64): every warp scans the m x W tile counts
