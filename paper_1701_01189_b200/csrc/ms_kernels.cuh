@@ -573,8 +573,8 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       }
       if (issued) bulk_commit();
     }
-    if (tid < 8u * m) {
-      const uint32_t b = tid >> 3, j = tid & 7u;
+    for (uint32_t t8 = tid; t8 < 8u * m; t8 += NT) {
+      const uint32_t b = t8 >> 3, j = t8 & 7u;
       const uint32_t len = s_run[2 * m + b];
       const uint32_t gs = s_run[m + b];
       const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);

@@ -83,7 +83,7 @@ def test_tile_size():
 
 
 @pytest.mark.parametrize("n", [T - 1, T, T + 1, 2 * T - 3, 3 * T + 5, 37 * T + 4097])
-@pytest.mark.parametrize("m", [2, 5, 32, 200, 256])
+@pytest.mark.parametrize("m", [2, 5, 32, 33, 64, 200, 256])
 @pytest.mark.parametrize("dist", [gen.DIST_UNIFORM, gen.DIST_SKEW, gen.DIST_BINOMIAL])
 def test_tile_boundaries_and_distributions(n, m, dist):
     ob, pb, gk = bucket_pair("delta", m)
