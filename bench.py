@@ -301,12 +301,12 @@ def run_ours(args, rank, world, local_rank):
         ms_step = float(t.item())
     n = run.n
     value = n * world / (ms_step * 1e-3) / 1e9  # all ranks' elements / max-over-ranks step time
-    # dominant kernel = postscan (KS); algorithmic bytes per launch: read + write of keys (+ values)
+    # dominant kernel = KF (kf_fused); algorithmic bytes per launch: read + write of keys (+ values)
     roofline = None
     if stages is not None:
         ks_bytes = n * (16 if wl["pairs"] else 8)
         achieved = ks_bytes / (stages["postscan"] * 1e-3) / 1e9
-        roofline = {"kernel": "ks_postscan", "bound": "hbm", "achieved": round(achieved, 1),
+        roofline = {"kernel": "kf_fused (KF: rank + reorder + scatter)", "bound": "hbm", "achieved": round(achieved, 1),
                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                     "traffic": load_traffic(f"{args.workload}_m{m}"),
                     "alg_bytes_per_launch": ks_bytes, "peak_source": peak_src,

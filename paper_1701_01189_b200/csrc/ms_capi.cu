@@ -232,8 +232,9 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.hdr = hdr;
   a.bucket_offsets = bucket_offsets;
   a.use_tma = (((uintptr_t)keys_in & 15u) == 0) && (!pairs || (((uintptr_t)vals_in & 15u) == 0));
-  // whole-run TMA stores for m <= 64 (long runs); per-element stores beyond
-  a.store_runs = m <= 64 && (((uintptr_t)keys_out & 15u) == 0) &&
+  // whole-run TMA bulk stores pay off when the average bucket run of a tile is
+  // >= 256 elements (measured: profiles/r01/); shorter runs use per-element stores
+  a.store_runs = m <= 64 && lo.T / m >= 256u && (((uintptr_t)keys_out & 15u) == 0) &&
                  (!pairs || (((uintptr_t)vals_out & 15u) == 0)) && !env_flag("MS_NO_RUN_STORES");
 
   if (n <= lo.T) {  // one subproblem: a single launch
