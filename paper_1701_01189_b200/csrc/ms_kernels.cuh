@@ -265,7 +265,7 @@ __host__ __device__ constexpr uint32_t kf_tile(bool pairs, int cls) {
 __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
   return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;
 }
-// Shared memory (bytes): 2 input stages | reordered tile | peer masks [2][W][m]
+// Shared memory (bytes): 2 input stages | reordered tile | peer masks [2 or 3][W][m]
 // | per-warp counts [W][m] | per-warp running slots [W][m] (m <= 64) | delta[m]
 // | run table [3][m] (m <= 64)
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
@@ -273,7 +273,7 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   const size_t T = kf_tile(pairs, cls), W = (size_t)kf_shape(pairs, cls).warps;
   const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  const size_t rows = cls == 2 ? 3 : 4;
+  const size_t rows = cls == 2 ? 3 : (cls == 1 ? 4 : 5);  // masks (2 or 3) + counts (+ slots)
   const size_t tables = cls == 2 ? 1 : 4;
   return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 +
          tables * mm * 4;
@@ -304,6 +304,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   uint32_t *crow = s_cnt + warp * re;
   uint32_t *mrow0 = s_mask + warp * re;        // window parity 0
   uint32_t *mrow1 = s_mask + (W + warp) * re;  // window parity 1
+  uint32_t *mrow2 = s_mask + (2 * W + warp) * re;  // m <= 32: windows i mod 3
   const uint32_t *in_k = s_in + wbase + lane;  // element i of this lane: in_k[32 i]
   const uint32_t *in_v = s_in + T + wbase + lane;
   uint32_t *out_k = s_out;
@@ -316,6 +317,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     for (uint32_t j = lane; j < m; j += 32) {
       mrow0[j] = 0u;
       mrow1[j] = 0u;
+      if constexpr (SCAN == 1) mrow2[j] = 0u;
       crow[j] = 0u;
     }
     __syncwarp();
@@ -354,6 +356,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   __syncthreads();
 
   uint32_t *brow = WSCAN ? s_base + warp * re : crow;  // this warp's running slot per bucket
+  uint32_t wrun = 0;  // SCAN == 1: lane b's running slot of bucket b
   if constexpr (WSCAN) {
     // ---- 2'. per-warp scan: this warp's first slot for bucket b is the tile
     //   base tb[b] (buckets before b) + counts of b in warps before this one
@@ -401,6 +404,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
         }
         const uint32_t adj = a.store_runs ? 4u * b + ((gs - tb) & 3u) : 0u;
         brow[b] = tb + colp[k] + adj;
+        if (k == 0) wrun = tb + colp[k] + adj;
         if (warp == 0) {
           if (a.store_runs) {
             s_run[b] = tb + adj;
@@ -528,6 +532,19 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
           c0 += __popc(vm) - nones;
         }
         c1 += nones;
+      } else if constexpr (SCAN == 1) {
+        // m <= 32: lane j keeps bucket j's running slot in a register and reads
+        // bucket j's mask to advance it; masks rotate over three rows so that one
+        // __syncwarp per window orders the ORs, the reads and the clears
+        uint32_t *mrow = (i % 3 == 0) ? mrow0 : ((i % 3 == 1) ? mrow1 : mrow2);
+        uint32_t *mprev = (i % 3 == 0) ? mrow2 : ((i % 3 == 1) ? mrow0 : mrow1);
+        if (valid) atomicOr(mrow + b, lanebit);
+        __syncwarp();
+        const uint32_t peers = valid ? mrow[b] : 0u;
+        const uint32_t mine = lane < m ? mrow[lane] : 0u;
+        slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
+        if (i > 0 && lane < m) mprev[lane] = 0u;  // every lane read the previous row last window
+        wrun += __popc(mine);
       } else {
         uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
         if (valid) atomicOr(mrow + b, lanebit);
@@ -630,7 +647,8 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
   uint32_t *s_out = stage0 + 2 * SW;
   uint32_t *s_mask = s_out + OS * (PAIRS ? 2u : 1u);
-  uint32_t *s_cnt = s_mask + 2 * W * mm;
+  constexpr uint32_t kMaskRows = SCAN == 1 ? 3 : 2;  // m <= 32: triple-buffered masks
+  uint32_t *s_cnt = s_mask + kMaskRows * W * mm;
   uint32_t *s_base = s_cnt + W * mm;  // WSCAN only
   uint32_t *s_delta = WSCAN ? s_base + W * mm : s_base;
   uint32_t *s_run = s_delta + mm;
