@@ -265,7 +265,8 @@ __host__ __device__ constexpr uint32_t kf_tile(bool pairs, int cls) {
 __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
   return m > 64 ? T : T + 4u * (m < 2 ? 2u : m) + 4u;
 }
-// Shared memory (bytes): 2 input stages | reordered tile | peer masks [2 or 3][W][m]
+// Shared memory (bytes): 3 tile stages (each padded to kf_out_slots, keys then values)
+// | peer masks [2 or 3][W][m]
 // | per-warp counts [W][m] | per-warp running slots [W][m] (m <= 64) | delta[m]
 // | run table [3][m] (m <= 64)
 __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
@@ -275,8 +276,7 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
   const size_t mm = m < 2 ? 2 : m;
   const size_t rows = cls == 2 ? 3 : (cls == 1 ? 4 : 5);  // masks (2 or 3) + counts (+ slots)
   const size_t tables = cls == 2 ? 1 : 4;
-  return 2 * T * k * 4 + (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 +
-         tables * mm * 4;
+  return 3 * (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 + tables * mm * 4;
 }
 
 // SCAN = 1 (m <= 32) / 2 (m <= 64): every warp scans the m x W tile counts
@@ -284,14 +284,12 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
 // (after ranking, after reordering); SCAN = 0: block-wide scan.
 // running[k] = next global position of bucket lane + 32k (SCAN > 0) or of
 // bucket tid (block scan).
-template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int SCAN, bool FULL,
-          class OnInputFree>
+template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int SCAN, bool FULL>
 __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &bp, uint32_t tile,
-                                           uint32_t tn, const uint32_t *s_in, uint32_t *s_out,
-                                           uint32_t OS, uint32_t *s_mask, uint32_t *s_cnt,
+                                           uint32_t tn, uint32_t *s_stage, uint32_t OS,
+                                           uint32_t *s_mask, uint32_t *s_cnt,
                                            uint32_t *s_base, uint32_t *s_delta, uint32_t *s_run,
-                                           uint32_t *s_wsum, uint32_t (&running)[2],
-                                           OnInputFree on_input_free) {
+                                           uint32_t *s_wsum, uint32_t (&running)[2]) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
   constexpr bool WSCAN = SCAN != 0;
@@ -305,10 +303,13 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   uint32_t *mrow0 = s_mask + warp * re;        // window parity 0
   uint32_t *mrow1 = s_mask + (W + warp) * re;  // window parity 1
   uint32_t *mrow2 = s_mask + (2 * W + warp) * re;  // m <= 32: windows i mod 3
-  const uint32_t *in_k = s_in + wbase + lane;  // element i of this lane: in_k[32 i]
-  const uint32_t *in_v = s_in + T + wbase + lane;
-  uint32_t *out_k = s_out;
-  uint32_t *out_v = s_out + OS;
+  // the tile is reordered in place: keys arrive in stage[0, T) (values in
+  // stage[OS, OS + T)), every lane holds its elements in registers from the count
+  // pass on, and the reordered tile is written back into the same stage
+  const uint32_t *in_k = s_stage + wbase + lane;  // element i of this lane: in_k[32 i]
+  const uint32_t *in_v = s_stage + OS + wbase + lane;
+  uint32_t *out_k = s_stage;
+  uint32_t *out_v = s_stage + OS;
   auto valid_at = [&](int i) { return FULL || wbase + (uint32_t)i * 32u + lane < tn; };
 
   // ---- 1. count pass: each warp's bucket counts (Eq.4 terms 2-3 need them
@@ -323,10 +324,15 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     __syncwarp();
   }
   bool derr = false;
-  {
-    uint32_t key[ITEMS];
+  uint32_t key[ITEMS];
+  uint32_t val[PAIRS ? ITEMS : 1];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) key[i] = valid_at(i) ? in_k[32 * i] : 0u;
+  for (int i = 0; i < ITEMS; ++i) key[i] = valid_at(i) ? in_k[32 * i] : 0u;
+  if constexpr (PAIRS) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) val[i] = valid_at(i) ? in_v[32 * i] : 0u;
+  }
+  {
     uint32_t c0 = 0, c1 = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -352,8 +358,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   if constexpr (KIND == kIdentity) {
     if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
   }
-  if (WSCAN && a.store_runs && warp == 0) bulk_wait_read();  // previous run stores left s_out
-  __syncthreads();
+  __syncthreads();  // every element is in registers: the stage may be overwritten
 
   uint32_t *brow = WSCAN ? s_base + warp * re : crow;  // this warp's running slot per bucket
   uint32_t wrun = 0;  // SCAN == 1: lane b's running slot of bucket b
@@ -453,7 +458,6 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       *c = run;
       run += v;
     }
-    if (a.store_runs && warp == 0) bulk_wait_read();  // previous tile's run stores left s_out
   }
   __syncthreads();
 
@@ -509,14 +513,11 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       base0 = brow[0];
       base1 = brow[1];
     }
-    uint32_t key_next = valid_at(0) ? in_k[0] : 0u;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const bool valid = valid_at(i);
-      const uint32_t key = key_next;
-      if (i + 1 < ITEMS) key_next = valid_at(i + 1) ? in_k[32 * (i + 1)] : 0u;
       if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: past the tail
-      const uint32_t b = bucket_of<KIND>(key, bp);
+      const uint32_t b = bucket_of<KIND>(key[i], bp);
       uint32_t slot;
       if constexpr (SMALLM) {
         // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
@@ -560,21 +561,21 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
         }
       }
       if (valid) {
-        out_k[slot] = key;
-        if constexpr (PAIRS) out_v[slot] = in_v[32 * i];
+        out_k[slot] = key[i];
+        if constexpr (PAIRS) out_v[slot] = val[i];
       }
     }
   }
   __syncthreads();
 
-  on_input_free();  // the input stage has been read for the last time
-
   if (a.store_runs) {
     // ---- 5a. one TMA bulk store per bucket run: the 16-byte aligned body by
     //          thread b, the <= 3 leading / trailing elements by threads 8b..8b+7
-    // run bodies: one TMA bulk store per bucket, issued by warp 0 (lane b, b + 32)
-    if (warp == 0) {
-      bool issued = false;
+    // run bodies: one TMA bulk store per bucket, issued by the producer warp
+    // (lane b, b + 32); every lane commits one bulk group per tile so that the
+    // producer can later wait for all but the newest before refilling a stage
+    if (warp == W - 1) {
+      bool fenced = false;
       for (uint32_t b = lane; b < m; b += 32) {
         const uint32_t len = s_run[2 * m + b];
         const uint32_t gs = s_run[m + b];
@@ -582,13 +583,13 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
         const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
         const uint32_t body = (len - head) & ~3u;
         if (body) {
-          fence_proxy_async_smem();
+          if (!fenced) fence_proxy_async_smem();  // generic smem writes -> async proxy
+          fenced = true;
           tma_store_1d(a.keys_out + gs + head, out_k + st + head, body * 4u);
           if constexpr (PAIRS) tma_store_1d(a.vals_out + gs + head, out_v + st + head, body * 4u);
-          issued = true;
         }
       }
-      if (issued) bulk_commit();
+      bulk_commit();
     }
     for (uint32_t t8 = tid; t8 < 8u * m; t8 += NT) {
       const uint32_t b = t8 >> 3, j = t8 & 7u;
@@ -637,22 +638,22 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   constexpr bool WSCAN = SCAN != 0;
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
-  constexpr uint32_t SW = T * (PAIRS ? 2u : 1u);  // words per stage
+  constexpr uint32_t kStages = 3;  // tile k lives in stage k % 3 from its TMA load to its stores
   extern __shared__ __align__(128) uint8_t kf_smem[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ uint32_t s_wsum[32];
   const uint32_t m = bp.m;
   const uint32_t mm = m < 2 ? 2 : m;
-  const uint32_t OS = kf_out_slots(T, m);
+  const uint32_t OS = kf_out_slots(T, m);         // words per stage region (keys; values after)
+  const uint32_t SW = OS * (PAIRS ? 2u : 1u);     // words per stage
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
-  uint32_t *s_out = stage0 + 2 * SW;
-  uint32_t *s_mask = s_out + OS * (PAIRS ? 2u : 1u);
+  uint32_t *s_mask = stage0 + kStages * SW;
   constexpr uint32_t kMaskRows = SCAN == 1 ? 3 : 2;  // m <= 32: triple-buffered masks
   uint32_t *s_cnt = s_mask + kMaskRows * W * mm;
   uint32_t *s_base = s_cnt + W * mm;  // WSCAN only
   uint32_t *s_delta = WSCAN ? s_base + W * mm : s_base;
   uint32_t *s_run = s_delta + mm;
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr uint32_t kProducer = NT - 32;  // lane 0 of the last warp issues the TMA loads
 
   uint32_t t0 = 0, t1 = 1;
@@ -662,18 +663,17 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     if (t0 >= t1) return;
   }
   auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
-  auto issue = [&](uint32_t t, int st) {  // one elected thread starts the TMA bulk copy
+  auto issue = [&](uint32_t t, uint32_t st) {  // one elected thread starts the TMA bulk copy
     if (tid == kProducer && t < t1 && a.use_tma && tile_n(t) == T) {
       uint32_t *dst = stage0 + st * SW;
       const uint64_t pol = policy_evict_first();
-      mbar_arrive_expect_tx(&bar[st], SW * 4u);
+      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
       tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
-      if constexpr (PAIRS) tma_load_1d(dst + T, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
+      if constexpr (PAIRS) tma_load_1d(dst + OS, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
     }
   };
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
     if (a.mode == kModeSingle) a.hdr[0] = 0u;
   }
   __syncthreads();
@@ -724,38 +724,40 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     }
   }
 
-  // ---- tiles of this range, in order, double-buffered TMA ----------------------
+  // ---- tiles of this range, in order; three stages rotate through
+  //      TMA load -> count/place in place -> stores ----------------------------
   uint32_t k = 0;
   for (uint32_t t = t0; t < t1; ++t, ++k) {
-    const int st = (int)(k & 1u);
-    uint32_t *s_in = stage0 + st * SW;
+    const uint32_t st = k % kStages;
+    uint32_t *s_stage = stage0 + st * SW;
     const uint32_t tn = tile_n(t);
     if (a.use_tma && tn == T) {
-      mbar_wait(&bar[st], (k >> 1) & 1u);
+      mbar_wait(&bar[st], (k / kStages) & 1u);
     } else {  // ragged last tile / unaligned input: plain loads
       for (uint32_t i = tid; i < tn; i += NT) {
-        s_in[i] = __ldg(a.keys_in + (size_t)t * T + i);
-        if constexpr (PAIRS) s_in[T + i] = __ldg(a.vals_in + (size_t)t * T + i);
+        s_stage[i] = __ldg(a.keys_in + (size_t)t * T + i);
+        if constexpr (PAIRS) s_stage[OS + i] = __ldg(a.vals_in + (size_t)t * T + i);
       }
       __syncthreads();
     }
-    // the producer refills this stage with tile t+2 as soon as it has been read
-    auto refill = [&]() {
-      if (tid == kProducer) {
-        fence_proxy_async_smem();  // generic-proxy smem accesses before the async-proxy write
-        issue(t + 2, st);
-      }
-    };
     if (tn == T)
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, true>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                      s_cnt, s_base, s_delta, s_run, s_wsum,
-                                                      running, refill);
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, true>(a, bp, t, tn, s_stage, OS, s_mask,
+                                                            s_cnt, s_base, s_delta, s_run, s_wsum,
+                                                            running);
     else
-      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, false>(a, bp, t, tn, s_in, s_out, OS, s_mask,
-                                                       s_cnt, s_base, s_delta, s_run, s_wsum,
-                                                       running, refill);
-    // no CTA barrier here: the next tile's shared structures are first written
-    // after barriers that every thread reaches only once done with this tile
+      kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, false>(a, bp, t, tn, s_stage, OS, s_mask,
+                                                             s_cnt, s_base, s_delta, s_run, s_wsum,
+                                                             running);
+    // refill stage (k+2) % 3 with tile t+2: its last user, tile t-1, was stored
+    // from it; the producer warp waits until those bulk stores have read it (all
+    // but its newest bulk group).  Plain loads/stores of tile t-1 from that stage
+    // finished before this tile's first barrier.
+    if (warp == W - 1) {
+      if (a.store_runs) bulk_wait_read_newest_pending();
+      __syncwarp();
+      if (lane == 0) fence_proxy_async_smem();
+      issue(t + 2, (k + 2) % kStages);
+    }
   }
   if (a.store_runs) bulk_wait_all();  // run stores complete before smem is released
 }
