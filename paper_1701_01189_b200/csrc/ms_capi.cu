@@ -47,9 +47,18 @@ uint32_t ctas_per_sm(uint32_t m, bool pairs) {
 // Workspace: [hdr 256 B][base 1280 B][R or H: L*m words][KG status: nchunks*m u64]
 // (the level-0 histogram R needs G <= L rows; the three-launch mode needs L rows of H).
 struct Layout {
-  size_t base, H, status, total;
-  uint32_t T, L, nchunks, C;
+  size_t base, H, status, meta, total;
+  uint32_t T, L, nchunks, C, MS;
 };
+
+// m <= 32: the prescan writes per-tile meta records (ms_meta.cuh) unless disabled
+bool use_meta(uint32_t m) {
+  static const bool off = [] {
+    const char *v = std::getenv("MS_NO_META");
+    return v && *v && std::strcmp(v, "0") != 0;
+  }();
+  return m <= 32 && !off;
+}
 
 Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   Layout lo{};
@@ -66,6 +75,11 @@ Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   lo.nchunks = (lo.L + lo.C - 1) / lo.C;
   lo.status = lo.H + align_up((size_t)lo.L * m * 8u);  // H (or R and its prefixes P)
   lo.total = lo.status + align_up((size_t)lo.nchunks * m * 8u);
+  lo.meta = lo.total;
+  if (m <= 32) {  // tile meta records (sized whether or not MS_NO_META is set)
+    lo.MS = meta_stride(meta_ms(m), kWarps);
+    lo.total = lo.meta + align_up((size_t)lo.L * lo.MS * 4u);
+  }
   return lo;
 }
 
@@ -182,6 +196,28 @@ cudaError_t tile_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t
   }
 }
 
+cudaError_t tile_meta(const Plan &pl, bool pairs, const uint32_t *keys, uint32_t n, uint32_t L,
+                      uint32_t K, uint32_t grid, uint32_t *meta, uint32_t *R, uint32_t *hdr,
+                      cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
+    case kDelta: return Launch<kDelta>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
+    case kRadix: return Launch<kRadix>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
+    case kTopBits: return Launch<kTopBits>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
+    default: return Launch<kDeltaShift>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
+  }
+}
+
+cudaError_t fused_meta(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::fused_meta(pairs, a, pl.bp, grid, s);
+    case kDelta: return Launch<kDelta>::fused_meta(pairs, a, pl.bp, grid, s);
+    case kRadix: return Launch<kRadix>::fused_meta(pairs, a, pl.bp, grid, s);
+    case kTopBits: return Launch<kTopBits>::fused_meta(pairs, a, pl.bp, grid, s);
+    default: return Launch<kDeltaShift>::fused_meta(pairs, a, pl.bp, grid, s);
+  }
+}
+
 cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
   switch (pl.kind) {
     case kIdentity: return Launch<kIdentity>::fused(pairs, a, pl.bp, grid, s);
@@ -283,9 +319,16 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
+  const bool meta_mode = use_meta(m);
+  uint32_t *meta = (uint32_t *)(w + lo.meta);
   stage_event(0, s);
-  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
+  if (meta_mode) {
+    if (counted(tile_meta(pl, pairs, keys_in, (uint32_t)n, lo.L, K, G, meta, H, hdr, s)) !=
+        cudaSuccess)
+      return MS_ERR_CUDA;
+  } else if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess) {
     return MS_ERR_CUDA;
+  }
   stage_event(1, s);
   uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
   if (counted(launch_level0_scan(H, P, base, G, m, s)) != cudaSuccess) return MS_ERR_CUDA;
@@ -295,7 +338,8 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.Tot = base;
   a.tiles_per_cta = K;
   a.num_ranges = G;
-  const cudaError_t e = counted(fused(pl, pairs, a, G, s));
+  a.meta = meta;
+  const cudaError_t e = counted(meta_mode ? fused_meta(pl, pairs, a, G, s) : fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
 }
@@ -315,7 +359,11 @@ ms_status radix_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
                 overlaps(keys_in, vals_out, n) || overlaps(vals_in, keys_out, n)))
     return MS_ERR_INVALID_VALUE;
   if (ws_bytes < ms_radix_sort_workspace_size(n, pairs)) return MS_ERR_WORKSPACE;
-  const size_t ms_bytes = ms_multisplit_workspace_size(n, 1u << r, pairs);
+  size_t ms_bytes = 0;  // widest multisplit workspace over the passes
+  for (int p = 0; p < passes; ++p) {
+    const size_t x = ms_multisplit_workspace_size(n, 1u << bits[p], pairs);
+    ms_bytes = x > ms_bytes ? x : ms_bytes;
+  }
   char *w = (char *)ws;
   uint32_t *alt_k = (uint32_t *)(w + align_up(ms_bytes));
   uint32_t *alt_v = pairs ? (uint32_t *)((char *)alt_k + align_up(n * 4u)) : nullptr;
@@ -413,7 +461,13 @@ int ms_radix_pass_schedule(uint32_t begin_bit, uint32_t end_bit, uint32_t r, uin
 }
 
 size_t ms_radix_sort_workspace_size(uint64_t n, int with_values) {
-  return align_up(ms_multisplit_workspace_size(n, 256, with_values)) + align_up(n * 4u) +
+  // the multisplit workspace of the widest pass over every digit width r = 1..8
+  size_t ms_ws = 0;
+  for (uint32_t r = 1; r <= 8; ++r) {
+    const size_t x = ms_multisplit_workspace_size(n, 1u << r, with_values);
+    ms_ws = x > ms_ws ? x : ms_ws;
+  }
+  return align_up(ms_ws) + align_up(n * 4u) +
          (with_values ? align_up(n * 4u) : 0u);
 }
 

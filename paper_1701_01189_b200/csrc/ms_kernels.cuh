@@ -236,6 +236,7 @@ struct KfArgs {
   const uint32_t *Tot;   // [m] bucket totals (kModeRange)
   const uint32_t *Gt;    // [num_tiles][m] column part of Eq.2 offsets (kModeTileG)
   const uint32_t *base;  // [m] bucket bases, first term of Eq.2 (kModeTileG)
+  const uint32_t *meta;  // [num_tiles][meta_stride] tile meta records from KM (kf_meta)
   uint32_t *hdr;         // [0] key-domain error flag
   uint32_t *bucket_offsets;
   int mode;

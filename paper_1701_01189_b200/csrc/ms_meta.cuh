@@ -1,0 +1,591 @@
+// ms_meta.cuh -- the m <= 32 pipeline with warp-level offsets computed in the
+// prescan (KM) instead of the postscan (KF):
+//
+//   KM  km_tile_meta (P:534-535 prescan, extended): for every tile l of its
+//       level-0 range and every warp slice w of the tile, the per-warp bucket
+//       counts c_{l,w}[j], then the tile-local exclusive scan in (bucket, warp)
+//       order S_l[j][w] = sum_{j'<j} h_{l}[j'] + sum_{w'<w} c_{l,w'}[j]
+//       (Eq.4 terms 2-3).  It writes them as one "tile meta" record
+//       per tile, and the range histogram R[c][j] for the level-0 scan (KR).
+//       KF accumulates the range-running prefix sum_{l'<l} h_{l'}[j] (Eq.3
+//       term 3) itself from the records' tile counts.
+//   KF  kf_meta: per tile, each warp reads its m slot bases from the meta
+//       record (TMA'd with the tile), ranks its windows (Eq.4 term 1) and
+//       places the keys in shared memory in place; one CTA barrier per tile,
+//       then the coalesced scatter of the bucket runs.
+//
+// Why (B200, measured in profiles/r01/s2_summary.md): the postscan is
+// issue-bound (43 thread-instructions per key, 52 % issue utilisation, 27 % of
+// warp samples parked at the post-count barrier) while the prescan streams at
+// ~5.5 TB/s with 77 % of its issue slots idle.  The count pass and the
+// redundant per-warp scan (16.5 instructions per key) move to the prescan;
+// the price is one meta record per tile, 16 m words, i.e. 0.25 B/key
+// written and read again at m = 32 (the paper recomputes instead, P:778
+// footnote, which was the right trade on a GPU whose postscan was not
+// issue-bound).
+#pragma once
+#include <type_traits>
+
+#include "ms_kernels.cuh"
+
+namespace ms {
+
+// meta record: [S: W x mS words, warp-major: S[w][j] at w*mS + j][pad to 16 B]; the
+// range-running prefix (Eq.3 term 3) is accumulated by KF from the tile counts
+__host__ __device__ constexpr uint32_t meta_stride(uint32_t mS, uint32_t W) {
+  return (mS * W + 3u) & ~3u;
+}
+__host__ __device__ constexpr uint32_t meta_ms(uint32_t m) { return m < 2 ? 2u : m; }
+
+// ============================================================================
+// KM: per-tile warp-slice counts -> tile meta records + range histogram.
+// CTA c handles tiles [c*K, min(L, (c+1)*K)) -- the same partition as KF.
+// Warp w of the CTA counts slice w of each tile: keys [l*T + w*SL, +SL).
+// ============================================================================
+// KM: keys-only tiles of T = 512 ITEMS words in a TMA ring of KS stages; the
+// CTA handles TPR tiles per round (one pair of CTA barriers per round).
+__host__ __device__ constexpr uint32_t km_stages(int items) { return items >= 16 ? 3u : 5u; }
+__host__ __device__ constexpr uint32_t km_tpr(int items) { return 1u; }
+__host__ __device__ inline size_t km_smem_bytes(uint32_t m, bool pairs) {
+  const int items = pairs ? 8 : 16;
+  return ((size_t)km_stages(items) * kThreads * items +
+          km_tpr(items) * (kWarps * meta_ms(m) + 32u)) * 4u;
+}
+
+template <int KIND, bool SMALLM, int ITEMS>
+__global__ void __launch_bounds__(kThreads, 2)
+    km_tile_meta(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
+                 uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
+                 uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  constexpr uint32_t W = kWarps;
+  constexpr uint32_t SL = 32u * ITEMS;  // keys per warp slice
+  constexpr uint32_t T = W * SL;
+  constexpr int NV = ITEMS / 4;         // uint4 per lane per slice
+  constexpr uint32_t KS = km_stages(ITEMS);
+  constexpr uint32_t TPR = km_tpr(ITEMS);
+  // stages [KS][T] | cnt[TPR][W][mS] | s_h[TPR][32]
+  extern __shared__ __align__(128) uint32_t km_smem[];
+  __shared__ __align__(8) uint64_t bar[KS];
+  griddep_launch_dependents();  // KR may be scheduled early (it waits for us)
+  const uint32_t m = bp.m, mS = SMALLM ? 2u : m;
+  const uint32_t MS = meta_stride(mS, W);
+  uint32_t *cnt = km_smem + KS * T;
+  uint32_t *s_h = cnt + TPR * W * mS;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sb = tid >> 4, sw = tid & 15;  // scan role: bucket sb, warp sw
+  if (blockIdx.x == 0 && tid == 0) hdr[0] = 0u;  // key-domain flag of this call (KF sets it)
+  for (uint32_t i = tid; i < TPR * W * mS; i += kThreads) cnt[i] = 0u;
+  const uint32_t t0 = blockIdx.x * tiles_per_cta;
+  const uint32_t t1 = min(num_tiles, t0 + tiles_per_cta);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0);
+  auto via_tma = [&](uint32_t t) { return aligned && (uint64_t)(t + 1) * T <= n; };
+  auto issue = [&](uint32_t t, uint32_t st) {
+    if (tid == 0 && t < t1 && via_tma(t)) {
+      mbar_arrive_expect_tx(&bar[st], T * 4u);
+      tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &bar[st], policy_evict_first());
+    }
+  };
+  if (tid == 0)
+    for (uint32_t i = 0; i < KS; ++i) mbar_init(&bar[i], 1);
+  __syncthreads();
+  for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
+  uint32_t running = 0;
+  for (uint32_t r0 = t0; r0 < t1; r0 += TPR) {
+    const uint32_t nr = min(TPR, t1 - r0);  // tiles in this round
+    // ---- counts of this warp's slice of every tile of the round -------------
+#pragma unroll
+    for (uint32_t j = 0; j < TPR; ++j) {
+      if (j < nr) {
+        const uint32_t t = r0 + j, k = t - t0, st = k % KS;
+        uint32_t ones = 0, nvalid = SL;
+        uint32_t *row = cnt + (j * W + warp) * mS;
+        if (via_tma(t)) {
+          mbar_wait(&bar[st], (k / KS) & 1u);
+          const uint4 *v = reinterpret_cast<const uint4 *>(km_smem + st * T + warp * SL);
+          uint4 q[NV];
+#pragma unroll
+          for (int u = 0; u < NV; ++u) q[u] = v[lane + 32u * (uint32_t)u];
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t b = bucket_of<KIND>(k4[e], bp);
+              if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
+            }
+          }
+        } else {  // ragged last tile / unaligned input
+          const uint64_t lo = (uint64_t)t * T + warp * SL;
+          const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
+          nvalid = hi > lo ? hi - (uint32_t)lo : 0u;
+          for (uint32_t i = (uint32_t)lo + lane; i < hi; i += 32u) {
+            const uint32_t b = bucket_of<KIND>(__ldg(keys + i), bp);
+            if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
+          }
+        }
+        if constexpr (SMALLM) {
+          ones = __reduce_add_sync(0xFFFFFFFFu, ones);
+          if (lane == 0) {
+            row[0] = nvalid - ones;
+            row[1] = ones;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // every warp has read the round's stages: refill them
+    if (tid == 0) fence_proxy_async_smem();
+    for (uint32_t j = 0; j < nr; ++j) issue(r0 + j + KS, (r0 + j - t0) % KS);
+    // ---- tile-local scans in (bucket, warp) order: thread (sb, sw) ------------
+    const bool act = sb < mS;
+    uint32_t cj[TPR], inj[TPR];
+#pragma unroll
+    for (uint32_t j = 0; j < TPR; ++j) {
+      const uint32_t c = (act && j < nr) ? cnt[(j * W + sw) * mS + sb] : 0u;
+      if (act && j < nr) cnt[(j * W + sw) * mS + sb] = 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o, 16);
+        if (sw >= (uint32_t)o) incl += y;
+      }
+      const uint32_t h = __shfl_sync(0xFFFFFFFFu, incl, 15, 16);  // tile count of bucket sb
+      if (act && sw == 0) s_h[j * 32 + sb] = h;
+      cj[j] = c;
+      inj[j] = incl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < TPR; ++j) {
+      if (j < nr) {
+        const uint32_t x = lane < mS ? s_h[j * 32 + lane] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
+          if (lane >= (uint32_t)o) xi += y;
+        }
+        const uint32_t tb = __shfl_sync(0xFFFFFFFFu, xi - x, sb & 31u);  // tile base of bucket sb
+        const uint32_t h = __shfl_sync(0xFFFFFFFFu, x, sb & 31u);
+        if (act) {
+          meta[(size_t)(r0 + j) * MS + sw * mS + sb] = tb + inj[j] - cj[j];
+          if (sw == 0) running += h;
+        }
+      }
+    }
+  }
+  if (sb < m && sw == 0) R[(size_t)blockIdx.x * m + sb] = running;
+}
+
+// Shared memory of kf_meta: 3 stages of [keys OS | values OS | meta MS] words,
+// peer masks [3][W][32], run tables [2][3][32] (or deltas [2][32]).
+__host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
+  const uint32_t T = kThreads * (pairs ? 8u : 16u);
+  const size_t SW = (size_t)kf_out_slots(T, m) * (pairs ? 2u : 1u) + meta_stride(meta_ms(m), kWarps);
+  return (3 * SW + 3 * kWarps * 32 + 3 * 3 * 32) * 4;
+}
+
+// ============================================================================
+// KF (meta mode): persistent CTA per level-0 range, tiles in order; 16
+// consumer warps rank and place, and (PROD) one producer warp does all TMA.
+//   consumer iteration k (tile t): per-warp setup from the tile meta; rank and
+//   place the keys held in registers into the stage, in place; load tile t+1's
+//   keys into registers; ONE barrier among the consumers.  All consumer warps
+//   load tile t+1's keys before that barrier, so the in-place placement of
+//   tile t+1 never overwrites a key that is still unread.
+//   PROD (whole-run TMA bulk stores): the consumers arrive on placed[k % 3];
+//   the producer warp waits for it, issues tile t's run stores, and refills
+//   the stage of tile t-1 (read by now) with tile t+2 -- the consumers never
+//   wait for a store or issue one.
+//   !PROD: after the barrier the last warp issues tile t's run stores (TMA
+//   bulk) and every thread stores run heads / tails, or (no run stores) every
+//   thread scatters its slots; then the stage of tile t-1 gets tile t+2.
+// ============================================================================
+// RANK (m > 2): 0 = peer masks by shared-memory atomicOr of the lane bit;
+//               1 = peer masks from ceil(log2 m) ballots of the bucket bits
+//                   (Alg.3): no shared-memory traffic, more ALU work;
+//               2 / 3 = ballots for every third / every second window, atomics
+//                   for the others (balances the shared-memory and ALU pipes);
+//               4 / 5 / 6 = as 0 / 2 / 3 with the atomic windows' masks taken
+//                   and cleared by one atomic exchange per bucket lane.
+template <int KIND, bool PAIRS, bool SMALLM, int ITEMS, int RANK, bool PROD>
+__global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(KfArgs a, BucketParams bp) {
+  constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
+  constexpr uint32_t T = NT * ITEMS;
+  constexpr uint32_t kStages = 3;
+  extern __shared__ __align__(128) uint8_t kf_smem[];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ __align__(8) uint64_t placed[kStages];  // PROD: tile placed, 512 arrivals
+  const uint32_t m = bp.m, mS = SMALLM ? 2u : m;
+  const uint32_t OS = kf_out_slots(T, m);
+  const uint32_t MS = meta_stride(mS, W);
+  const uint32_t MO = OS * (PAIRS ? 2u : 1u);  // meta offset inside a stage
+  const uint32_t SW = MO + MS;                 // words per stage
+  uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
+  uint32_t *s_mask = stage0 + kStages * SW;  // [3][W][32]
+  uint32_t *s_tab = s_mask + 3 * W * 32;     // [3][3][32] run tables / deltas per stage
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t lt = lanemask_lt(), lanebit = 1u << lane;
+  // the thread that issues the TMA loads: lane 0 of the producer warp (PROD) or
+  // of the last consumer warp
+  constexpr uint32_t kProducer = PROD ? NT : NT - 32;
+  const uint32_t logm = 32u - __clz(m - 1u);  // bucket bits (RANK 1)
+
+  const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
+  const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
+  if (t0 >= t1) return;
+  auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
+  auto via_tma = [&](uint32_t t) { return a.use_tma && tile_n(t) == T; };
+  // one elected thread starts the TMA bulk copies of a tile: the input data
+  // (may run before griddep_wait: the inputs predate KM) and the meta record
+  // (written by KM: only after griddep_wait); one mbarrier transaction count
+  auto issue_data = [&](uint32_t t, uint32_t st) {
+    if (tid == kProducer && t < t1 && via_tma(t)) {
+      uint32_t *dst = stage0 + st * SW;
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u) + MS * 4u);
+      tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
+      if constexpr (PAIRS) tma_load_1d(dst + OS, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
+    }
+  };
+  auto issue_meta = [&](uint32_t t, uint32_t st) {
+    if (tid == kProducer && t < t1 && via_tma(t))
+      tma_load_1d(stage0 + st * SW + MO, a.meta + (size_t)t * MS, MS * 4u, &bar[st],
+                  policy_evict_first());
+  };
+  auto issue = [&](uint32_t t, uint32_t st) {
+    issue_data(t, st);
+    issue_meta(t, st);
+  };
+  if (tid == 0) {
+    for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
+    if constexpr (PROD)
+      for (uint32_t i = 0; i < kStages; ++i) mbar_init(&placed[i], NT);
+  }
+  __syncthreads();
+  issue_data(t0, 0);
+  issue_data(t0 + 1, 1);
+  if constexpr (PROD) {
+    if (warp == W) {
+      // ======================= producer warp =================================
+      griddep_wait();  // meta records are complete
+      issue_meta(t0, 0);
+      issue_meta(t0 + 1, 1);
+      uint32_t k = 0;
+      for (uint32_t t = t0; t < t1; ++t, ++k) {
+        const uint32_t st = k % kStages;
+        uint32_t *s_stage = stage0 + st * SW;
+        const uint32_t *tab = s_tab + st * 96u;
+        // refill the stage of tile t-1 with tile t+2 as soon as tile t-1's bulk
+        // stores have read it, before tile t's stores are queued behind it
+        bulk_wait_read();
+        __syncwarp();
+        if (lane == 0) fence_proxy_async_smem();
+        issue(t + 2, (k + 2) % kStages);
+        mbar_wait(&placed[st], (k / kStages) & 1u);
+        // one TMA bulk store per bucket run body (16-byte aligned), then the
+        // <= 3 leading / trailing elements of every run with plain stores
+        if (lane < m) {
+          const uint32_t len = tab[64 + lane], gs = tab[32 + lane], st0 = tab[lane];
+          const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+          const uint32_t body = (len - head) & ~3u;
+          if (body) {
+            fence_proxy_async_smem();
+            tma_store_1d(a.keys_out + gs + head, s_stage + st0 + head, body * 4u);
+            if constexpr (PAIRS) tma_store_1d(a.vals_out + gs + head, s_stage + OS + st0 + head, body * 4u);
+          }
+        }
+        bulk_commit();
+        for (uint32_t x = lane; x < 8u * m; x += 32u) {
+          const uint32_t b = x >> 3, j = x & 7u;
+          const uint32_t len = tab[64 + b], gs = tab[32 + b];
+          const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+          const uint32_t tail = (len - head) & 3u;
+          uint32_t e = 0xFFFFFFFFu;
+          if (j < 4u) {
+            if (j < head) e = j;
+          } else if (j - 4u < tail) {
+            e = len - tail + (j - 4u);
+          }
+          if (e != 0xFFFFFFFFu) {
+            const uint32_t sidx = tab[b] + e;
+            a.keys_out[gs + e] = s_stage[sidx];
+            if constexpr (PAIRS) a.vals_out[gs + e] = s_stage[OS + sidx];
+          }
+        }
+      }
+      bulk_wait_all();  // run stores complete before smem is released
+      return;
+    }
+  }
+
+  // keys (values) of one tile -> registers: lane l of warp w holds element
+  // w*32*ITEMS + 32 i + l.  TMA tiles come from the stage, others from global
+  // (and their meta record is copied into the stage by plain loads).
+  uint32_t key[ITEMS];
+  uint32_t val[PAIRS ? ITEMS : 1];
+  const uint32_t wbase = warp * (ITEMS * 32);
+  auto load_tile = [&](uint32_t t, uint32_t k) {
+    const uint32_t st = k % kStages;
+    uint32_t *s = stage0 + st * SW;
+    const uint32_t tn = tile_n(t);
+    if (via_tma(t)) {
+      mbar_wait(&bar[st], (k / kStages) & 1u);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) key[i] = s[wbase + 32 * i + lane];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) val[i] = s[OS + wbase + 32 * i + lane];
+      }
+    } else {
+      const size_t g = (size_t)t * T;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const uint32_t e = wbase + 32 * i + lane;
+        key[i] = e < tn ? __ldg(a.keys_in + g + e) : 0u;
+        if constexpr (PAIRS) val[i] = e < tn ? __ldg(a.vals_in + g + e) : 0u;
+      }
+      for (uint32_t i = tid; i < MS; i += NT) s[MO + i] = __ldg(a.meta + (size_t)t * MS + i);
+    }
+  };
+
+  // ---- level-0 offsets (Eq.3 terms 1-2): every warp forms the global start of
+  // the range's bucket lane, base[b] + P[c][b] (KR scanned the m x G matrix)
+  griddep_wait();  // KR (and KM before it) complete: meta records, prefixes, totals
+  issue_meta(t0, 0);
+  issue_meta(t0 + 1, 1);
+  uint32_t gbase = 0, grun = 0;
+  {
+    const uint32_t tot = lane < m ? __ldg(a.Tot + lane) : 0u;
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane < m) {
+      gbase = incl - tot + __ldg(a.R + (size_t)blockIdx.x * m + lane);
+      if (blockIdx.x == 0 && warp == 0 && a.bucket_offsets) {
+        a.bucket_offsets[lane] = incl - tot;
+        if (lane == m - 1) a.bucket_offsets[m] = incl;
+      }
+    }
+  }
+  load_tile(t0, 0);
+  named_barrier_sync(1, NT);
+
+  uint32_t *mrow0 = s_mask + warp * 32, *mrow1 = s_mask + (W + warp) * 32,
+           *mrow2 = s_mask + (2 * W + warp) * 32;
+  uint32_t k = 0;
+  for (uint32_t t = t0; t < t1; ++t, ++k) {
+    const uint32_t st = k % kStages;
+    uint32_t *s_stage = stage0 + st * SW;
+    const uint32_t *rec = s_stage + MO;
+    const uint32_t tn = tile_n(t);
+    const bool full = tn == T;
+    uint32_t *tab = s_tab + st * 96u;
+
+    // ---- per-warp setup from the meta record (lane b = bucket b) -------------
+    // slot of this warp's first bucket-b key = S[b][warp] (+ run padding adj[b]
+    // so that the run starts congruent mod 4 with its global destination)
+    uint32_t wrun = 0;
+    if (lane < m) {
+      const uint32_t sbw = rec[warp * mS + lane];
+      const uint32_t tb = rec[lane];
+      const uint32_t te = lane + 1 < m ? rec[lane + 1] : tn;
+      const uint32_t gs = gbase + grun;  // Eq.3 term 3: tiles before this one in the range
+      grun += te - tb;
+      const uint32_t adj = a.store_runs ? 4u * lane + ((gs - tb) & 3u) : 0u;
+      wrun = sbw + adj;
+      if (warp == W - 1) {
+        if (a.store_runs) {
+          tab[lane] = tb + adj;
+          tab[32 + lane] = gs;
+          tab[64 + lane] = te - tb;
+        } else {
+          tab[lane] = gs - tb;
+        }
+      }
+    }
+    if constexpr (!SMALLM && RANK != 1) {
+      mrow0[lane] = 0u;
+      mrow1[lane] = 0u;
+      mrow2[lane] = 0u;
+    }
+    __syncwarp();
+
+    // ---- rank and place (Eq.4 term 1 + this warp's running slot) -------------
+    bool derr = false;
+    auto place = [&](auto full_c) {
+      constexpr bool FULL = decltype(full_c)::value;
+      uint32_t base0 = 0, base1 = 0, c0 = 0, c1 = 0;
+      if constexpr (SMALLM) {
+        base0 = __shfl_sync(0xFFFFFFFFu, wrun, 0);
+        base1 = __shfl_sync(0xFFFFFFFFu, wrun, 1);
+      }
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const bool valid = FULL || wbase + (uint32_t)i * 32u + lane < tn;
+        if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform: past the tail
+        const uint32_t b = bucket_of<KIND>(key[i], bp);
+        if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+        uint32_t slot;
+        if constexpr (SMALLM) {
+          // m <= 2: one ballot gives every peer mask (Alg.2/3 with log2 m = 1)
+          const uint32_t ones = __ballot_sync(0xFFFFFFFFu, valid && b != 0u);
+          const uint32_t ones_below = __popc(ones & lt);
+          const uint32_t nones = __popc(ones);
+          if (FULL) {
+            slot = b ? base1 + c1 + ones_below : base0 + c0 + lane - ones_below;
+            c0 += 32u - nones;
+          } else {
+            const uint32_t vm = __ballot_sync(0xFFFFFFFFu, valid);
+            slot = b ? base1 + c1 + ones_below : base0 + c0 + __popc(vm & ~ones & lt);
+            c0 += __popc(vm) - nones;
+          }
+          c1 += nones;
+        } else if (RANK == 1 || ((RANK == 2 || RANK == 5) && i % 3 == 2) ||
+                   ((RANK == 3 || RANK == 6) && (i & 1))) {
+          // ballot voting on the bucket bits (Alg.3): lane j forms the mask of
+          // the lanes whose bucket is j (its own lane bits select vote or ~vote);
+          // a key with bucket b fetches lane b's mask and running slot
+          uint32_t mine = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+          for (uint32_t kb = 0; kb < 5; ++kb) {
+            if (kb < logm) {
+              const uint32_t v = __ballot_sync(0xFFFFFFFFu, (b >> kb) & 1u);
+              mine &= ((lane >> kb) & 1u) ? v : ~v;
+            }
+          }
+          const uint32_t peers = __shfl_sync(0xFFFFFFFFu, mine, b);
+          slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
+          wrun += __popc(mine);
+          if constexpr (RANK == 2 || RANK == 3) {  // mixed: keep the atomic windows' mask rotation
+            uint32_t *mprev = (i % 3 == 0) ? mrow2 : ((i % 3 == 1) ? mrow0 : mrow1);
+            __syncwarp();
+            if (i > 0 && lane < m) mprev[lane] = 0u;
+          }
+        } else if constexpr (RANK >= 4) {
+          // peer masks by one shared-memory OR of the lane bit; lane j takes
+          // bucket j's mask and clears it with one atomic exchange, the key of
+          // bucket b gets its peers and running slot from lane b by shuffles.
+          // Two rows alternate over the atomic windows, one __syncwarp each.
+          const int r = RANK == 4 ? (i & 1) : (RANK == 5 ? (i % 3) : ((i >> 1) & 1));
+          uint32_t *mrow = r ? mrow1 : mrow0;
+          if (valid) atomicOr(mrow + b, lanebit);
+          __syncwarp();
+          const uint32_t mine = atomicExch(mrow + lane, 0u);  // lanes >= m: an unused, zero word
+          const uint32_t peers = __shfl_sync(0xFFFFFFFFu, mine, b);
+          slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
+          wrun += __popc(mine);
+        } else {
+          // peer masks by one shared-memory OR of the lane bit (Alg.3's ballot
+          // voting in one instruction); lane j keeps bucket j's running slot;
+          // three mask rows rotate so one __syncwarp per window suffices
+          uint32_t *mrow = (i % 3 == 0) ? mrow0 : ((i % 3 == 1) ? mrow1 : mrow2);
+          uint32_t *mprev = (i % 3 == 0) ? mrow2 : ((i % 3 == 1) ? mrow0 : mrow1);
+          if (valid) atomicOr(mrow + b, lanebit);
+          __syncwarp();
+          const uint32_t peers = valid ? mrow[b] : 0u;
+          const uint32_t mine = lane < m ? mrow[lane] : 0u;
+          slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
+          if (i > 0 && lane < m) mprev[lane] = 0u;
+          wrun += __popc(mine);
+        }
+        if (valid) {
+          s_stage[slot] = key[i];
+          if constexpr (PAIRS) s_stage[OS + slot] = val[i];
+        }
+      }
+    };
+    if (full)
+      place(std::true_type{});
+    else
+      place(std::false_type{});
+    if constexpr (KIND == kIdentity) {
+      if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
+    }
+    if constexpr (PROD) {
+      mbar_arrive(&placed[st]);  // tile t placed: the producer may store it
+      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      named_barrier_sync(1, NT);
+    } else if (a.store_runs) {
+      // ---- next tile's keys into registers before the barrier -----------------
+      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      named_barrier_sync(1, NT);
+      // ---- run stores of tile t: one TMA bulk store per run body by the last
+      // warp, the <= 3 leading / trailing elements by threads 8b .. 8b+7
+      if (warp == W - 1) {
+        if (lane < m) {
+          const uint32_t len = tab[64 + lane], gs = tab[32 + lane], st0 = tab[lane];
+          const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+          const uint32_t body = (len - head) & ~3u;
+          if (body) {
+            fence_proxy_async_smem();
+            tma_store_1d(a.keys_out + gs + head, s_stage + st0 + head, body * 4u);
+            if constexpr (PAIRS) tma_store_1d(a.vals_out + gs + head, s_stage + OS + st0 + head, body * 4u);
+          }
+        }
+        bulk_commit();
+      }
+      if (tid < 8u * m) {
+        const uint32_t b = tid >> 3, j = tid & 7u;
+        const uint32_t len = tab[64 + b], gs = tab[32 + b];
+        const uint32_t head = min(len, (4u - (gs & 3u)) & 3u);
+        const uint32_t tail = (len - head) & 3u;
+        uint32_t e = 0xFFFFFFFFu;
+        if (j < 4u) {
+          if (j < head) e = j;
+        } else if (j - 4u < tail) {
+          e = len - tail + (j - 4u);
+        }
+        if (e != 0xFFFFFFFFu) {
+          const uint32_t sidx = tab[b] + e;
+          a.keys_out[gs + e] = s_stage[sidx];
+          if constexpr (PAIRS) a.vals_out[gs + e] = s_stage[OS + sidx];
+        }
+      }
+      // ---- refill the stage of tile t-1 with tile t+2 once its bulk stores
+      // have read it (all groups but the newest)
+      if (warp == W - 1) {
+        bulk_wait_read_newest_pending();
+        __syncwarp();
+        if (lane == 0) fence_proxy_async_smem();
+        issue(t + 2, (k + 2) % kStages);
+      }
+    } else {
+      // ---- next tile's keys into registers before the barrier -----------------
+      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      named_barrier_sync(1, NT);
+      // ---- coalesced scatter of tile t: slot s of bucket b -> delta[b] + s ----
+      const uint32_t s0 = wbase + lane;
+      uint32_t kk[ITEMS], pos[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) kk[i] = s_stage[s0 + 32 * i];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * i;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (full || s0 + 32 * i < tn) a.keys_out[pos[i]] = kk[i];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) kk[i] = s_stage[OS + s0 + 32 * i];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          if (full || s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
+      }
+      // ---- refill the stage of tile t-1 with tile t+2 (its loads and stores
+      // finished before this tile's barrier)
+      if (warp == W - 1) {
+        __syncwarp();
+        if (lane == 0) fence_proxy_async_smem();
+        issue(t + 2, (k + 2) % kStages);
+      }
+    }
+  }
+  if constexpr (!PROD) {
+    if (a.store_runs) bulk_wait_all();  // run stores complete before smem is released
+  }
+}
+
+}  // namespace ms
