@@ -331,6 +331,17 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
   stage_event(1, s);
   uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
+  if (meta_mode) {  // KF reduces the range histograms itself (no KR)
+    stage_event(2, s);
+    a.mode = kModeRange;
+    a.R = H;
+    a.tiles_per_cta = K;
+    a.num_ranges = G;
+    a.meta = meta;
+    const cudaError_t e = counted(fused_meta(pl, pairs, a, G, s));
+    stage_event(3, s);
+    return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+  }
   if (counted(launch_level0_scan(H, P, base, G, m, s)) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
@@ -338,8 +349,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.Tot = base;
   a.tiles_per_cta = K;
   a.num_ranges = G;
-  a.meta = meta;
-  const cudaError_t e = counted(meta_mode ? fused_meta(pl, pairs, a, G, s) : fused(pl, pairs, a, G, s));
+  const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
 }

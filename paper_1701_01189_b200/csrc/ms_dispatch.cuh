@@ -163,7 +163,7 @@ static cudaError_t kfm_go2(const KfArgs &a, const BucketParams &bp, uint32_t gri
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;  // always after our own KR
+  cfg.numAttrs = 1;  // always right after our own KM
   return cudaLaunchKernelEx(&cfg, kern, a, bp);
 }
 

@@ -349,14 +349,36 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     }
   };
 
-  // ---- level-0 offsets (Eq.3 terms 1-2): every warp forms the global start of
-  // the range's bucket lane, base[b] + P[c][b] (KR scanned the m x G matrix)
-  griddep_wait();  // KR (and KM before it) complete: meta records, prefixes, totals
+  // ---- level-0 offsets (Eq.3 terms 1-2 with L_0 = G), no separate scan
+  // kernel: the CTA reduces the G x m range histograms R (written by KM) to
+  // its prefix P[c][b] = sum_{c'<c} R[c'][b] and the totals Tot[b]; every warp
+  // then forms base[b] + P[c][b] for its bucket lanes.  R is G m words, read
+  // from L2 (11 MB in all at m = 32, G = 296).
+  griddep_wait();  // KM complete: meta records and range histograms
   issue_meta(t0, 0);
   issue_meta(t0 + 1, 1);
   uint32_t gbase = 0, grun = 0;
   {
-    const uint32_t tot = lane < m ? __ldg(a.Tot + lane) : 0u;
+    uint32_t *red = s_mask;  // [2][16][32] scratch (the mask rows are zeroed per tile)
+    const uint32_t G = a.num_ranges, c = blockIdx.x;
+    uint32_t pre = 0, tot = 0;
+    if (lane < m) {
+      for (uint32_t r = warp; r < G; r += W) {
+        const uint32_t v = __ldg(a.R + (size_t)r * m + lane);
+        tot += v;
+        pre += r < c ? v : 0u;
+      }
+    }
+    red[warp * 32 + lane] = pre;
+    red[(W + warp) * 32 + lane] = tot;
+    named_barrier_sync(1, NT);
+    pre = 0;
+    tot = 0;
+#pragma unroll
+    for (uint32_t g = 0; g < W; ++g) {
+      pre += red[g * 32 + lane];
+      tot += red[(W + g) * 32 + lane];
+    }
     uint32_t incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -364,8 +386,8 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       if (lane >= (uint32_t)o) incl += y;
     }
     if (lane < m) {
-      gbase = incl - tot + __ldg(a.R + (size_t)blockIdx.x * m + lane);
-      if (blockIdx.x == 0 && warp == 0 && a.bucket_offsets) {
+      gbase = incl - tot + pre;
+      if (c == 0 && warp == 0 && a.bucket_offsets) {
         a.bucket_offsets[lane] = incl - tot;
         if (lane == m - 1) a.bucket_offsets[m] = incl;
       }
