@@ -132,14 +132,14 @@ cudaError_t Launch<KIND>::tile_meta(bool pairs, const uint32_t *keys, uint32_t n
   }
   if (bp.m <= 2) {
     if (pairs)
-      km_tile_meta<KIND, true, 8><<<grid, kThreads, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, true, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
     else
-      km_tile_meta<KIND, true, 16><<<grid, kThreads, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, true, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
   } else {
     if (pairs)
-      km_tile_meta<KIND, false, 8><<<grid, kThreads, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, false, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
     else
-      km_tile_meta<KIND, false, 16><<<grid, kThreads, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, false, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
   }
   return cudaGetLastError();
 }

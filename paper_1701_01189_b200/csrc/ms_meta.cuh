@@ -42,18 +42,19 @@ __host__ __device__ constexpr uint32_t meta_ms(uint32_t m) { return m < 2 ? 2u :
 // CTA c handles tiles [c*K, min(L, (c+1)*K)) -- the same partition as KF.
 // Warp w of the CTA counts slice w of each tile: keys [l*T + w*SL, +SL).
 // ============================================================================
-// KM: keys-only tiles of T = 512 ITEMS words in a TMA ring of KS stages; the
-// CTA handles TPR tiles per round (one pair of CTA barriers per round).
+// KM: keys-only tiles of T = 512 ITEMS words in a TMA ring of KS stages.
+// 16 counting warps (one slice of each tile each) and one scan warp that owns
+// the TMA ring and turns each tile's W x m counts into its meta record; the
+// two roles hand over through mbarriers (count buffers double-buffered by tile
+// parity), so no counting warp ever waits at a CTA barrier.
 __host__ __device__ constexpr uint32_t km_stages(int items) { return items >= 16 ? 3u : 5u; }
-__host__ __device__ constexpr uint32_t km_tpr(int items) { return 1u; }
 __host__ __device__ inline size_t km_smem_bytes(uint32_t m, bool pairs) {
   const int items = pairs ? 8 : 16;
-  return ((size_t)km_stages(items) * kThreads * items +
-          km_tpr(items) * (kWarps * meta_ms(m) + 32u)) * 4u;
+  return ((size_t)km_stages(items) * kThreads * items + 2u * kWarps * meta_ms(m)) * 4u;
 }
 
 template <int KIND, bool SMALLM, int ITEMS>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads + 32, 2)
     km_tile_meta(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
                  uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
@@ -62,119 +63,120 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr uint32_t T = W * SL;
   constexpr int NV = ITEMS / 4;         // uint4 per lane per slice
   constexpr uint32_t KS = km_stages(ITEMS);
-  constexpr uint32_t TPR = km_tpr(ITEMS);
-  // stages [KS][T] | cnt[TPR][W][mS] | s_h[TPR][32]
-  extern __shared__ __align__(128) uint32_t km_smem[];
-  __shared__ __align__(8) uint64_t bar[KS];
-  griddep_launch_dependents();  // KR may be scheduled early (it waits for us)
+  extern __shared__ __align__(128) uint32_t km_smem[];  // stages [KS][T] | cnt[2][W][mS]
+  __shared__ __align__(8) uint64_t full[KS];
+  __shared__ __align__(8) uint64_t cfull[2];   // counts of a tile complete (512 arrivals)
+  __shared__ __align__(8) uint64_t cempty[2];  // counts consumed and zeroed (32 arrivals)
+  griddep_launch_dependents();  // KF may start its prologue (it waits for our completion)
   const uint32_t m = bp.m, mS = SMALLM ? 2u : m;
   const uint32_t MS = meta_stride(mS, W);
   uint32_t *cnt = km_smem + KS * T;
-  uint32_t *s_h = cnt + TPR * W * mS;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t sb = tid >> 4, sw = tid & 15;  // scan role: bucket sb, warp sw
   if (blockIdx.x == 0 && tid == 0) hdr[0] = 0u;  // key-domain flag of this call (KF sets it)
-  for (uint32_t i = tid; i < TPR * W * mS; i += kThreads) cnt[i] = 0u;
+  for (uint32_t i = tid; i < 2 * W * mS; i += blockDim.x) cnt[i] = 0u;
   const uint32_t t0 = blockIdx.x * tiles_per_cta;
   const uint32_t t1 = min(num_tiles, t0 + tiles_per_cta);
   const bool aligned = ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0);
   auto via_tma = [&](uint32_t t) { return aligned && (uint64_t)(t + 1) * T <= n; };
-  auto issue = [&](uint32_t t, uint32_t st) {
-    if (tid == 0 && t < t1 && via_tma(t)) {
-      mbar_arrive_expect_tx(&bar[st], T * 4u);
-      tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &bar[st], policy_evict_first());
-    }
-  };
-  if (tid == 0)
-    for (uint32_t i = 0; i < KS; ++i) mbar_init(&bar[i], 1);
-  __syncthreads();
-  for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
-  uint32_t running = 0;
-  for (uint32_t r0 = t0; r0 < t1; r0 += TPR) {
-    const uint32_t nr = min(TPR, t1 - r0);  // tiles in this round
-    // ---- counts of this warp's slice of every tile of the round -------------
-#pragma unroll
-    for (uint32_t j = 0; j < TPR; ++j) {
-      if (j < nr) {
-        const uint32_t t = r0 + j, k = t - t0, st = k % KS;
-        uint32_t ones = 0, nvalid = SL;
-        uint32_t *row = cnt + (j * W + warp) * mS;
-        if (via_tma(t)) {
-          mbar_wait(&bar[st], (k / KS) & 1u);
-          const uint4 *v = reinterpret_cast<const uint4 *>(km_smem + st * T + warp * SL);
-          uint4 q[NV];
-#pragma unroll
-          for (int u = 0; u < NV; ++u) q[u] = v[lane + 32u * (uint32_t)u];
-#pragma unroll
-          for (int u = 0; u < NV; ++u) {
-            const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t b = bucket_of<KIND>(k4[e], bp);
-              if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
-            }
-          }
-        } else {  // ragged last tile / unaligned input
-          const uint64_t lo = (uint64_t)t * T + warp * SL;
-          const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
-          nvalid = hi > lo ? hi - (uint32_t)lo : 0u;
-          for (uint32_t i = (uint32_t)lo + lane; i < hi; i += 32u) {
-            const uint32_t b = bucket_of<KIND>(__ldg(keys + i), bp);
-            if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
-          }
-        }
-        if constexpr (SMALLM) {
-          ones = __reduce_add_sync(0xFFFFFFFFu, ones);
-          if (lane == 0) {
-            row[0] = nvalid - ones;
-            row[1] = ones;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // every warp has read the round's stages: refill them
-    if (tid == 0) fence_proxy_async_smem();
-    for (uint32_t j = 0; j < nr; ++j) issue(r0 + j + KS, (r0 + j - t0) % KS);
-    // ---- tile-local scans in (bucket, warp) order: thread (sb, sw) ------------
-    const bool act = sb < mS;
-    uint32_t cj[TPR], inj[TPR];
-#pragma unroll
-    for (uint32_t j = 0; j < TPR; ++j) {
-      const uint32_t c = (act && j < nr) ? cnt[(j * W + sw) * mS + sb] : 0u;
-      if (act && j < nr) cnt[(j * W + sw) * mS + sb] = 0u;
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o, 16);
-        if (sw >= (uint32_t)o) incl += y;
-      }
-      const uint32_t h = __shfl_sync(0xFFFFFFFFu, incl, 15, 16);  // tile count of bucket sb
-      if (act && sw == 0) s_h[j * 32 + sb] = h;
-      cj[j] = c;
-      inj[j] = incl;
-    }
-    __syncthreads();
-#pragma unroll
-    for (uint32_t j = 0; j < TPR; ++j) {
-      if (j < nr) {
-        const uint32_t x = lane < mS ? s_h[j * 32 + lane] : 0u;
-        uint32_t xi = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xi, o);
-          if (lane >= (uint32_t)o) xi += y;
-        }
-        const uint32_t tb = __shfl_sync(0xFFFFFFFFu, xi - x, sb & 31u);  // tile base of bucket sb
-        const uint32_t h = __shfl_sync(0xFFFFFFFFu, x, sb & 31u);
-        if (act) {
-          meta[(size_t)(r0 + j) * MS + sw * mS + sb] = tb + inj[j] - cj[j];
-          if (sw == 0) running += h;
-        }
-      }
+  if (tid == 0) {
+    for (uint32_t i = 0; i < KS; ++i) mbar_init(&full[i], 1);
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(&cfull[i], kThreads);
+      mbar_init(&cempty[i], 32);
     }
   }
-  if (sb < m && sw == 0) R[(size_t)blockIdx.x * m + sb] = running;
+  __syncthreads();
+
+  if (warp == W) {
+    // ============================ scan warp ===================================
+    auto issue = [&](uint32_t t, uint32_t st) {
+      if (lane == 0 && t < t1 && via_tma(t)) {
+        mbar_arrive_expect_tx(&full[st], T * 4u);
+        tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], policy_evict_first());
+      }
+    };
+    for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
+    uint32_t running = 0;  // range count of bucket lane
+    uint32_t k = 0;
+    for (uint32_t t = t0; t < t1; ++t, ++k) {
+      const uint32_t p = k & 1u;
+      mbar_wait(&cfull[p], (k >> 1) & 1u);
+      // every counting warp has read its slice of stage k % KS: refill it
+      if (lane == 0) fence_proxy_async_smem();
+      issue(t + KS, k % KS);
+      // column of bucket lane: exclusive prefix over the warps, tile count h
+      uint32_t *c = cnt + p * W * mS;
+      uint32_t col[W];
+      uint32_t h = 0;
+#pragma unroll
+      for (uint32_t w = 0; w < W; ++w) {
+        const uint32_t x = lane < mS ? c[w * mS + lane] : 0u;
+        col[w] = h;
+        h += x;
+      }
+#pragma unroll
+      for (uint32_t w = 0; w < W; ++w)
+        if (lane < mS) c[w * mS + lane] = 0u;
+      uint32_t incl = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      const uint32_t tb = incl - h;  // tile base of bucket lane
+      if (lane < mS) {
+        uint32_t *rec = meta + (size_t)t * MS;
+#pragma unroll
+        for (uint32_t w = 0; w < W; ++w) rec[w * mS + lane] = tb + col[w];
+      }
+      running += h;
+      __syncwarp();
+      mbar_arrive(&cempty[p]);
+    }
+    if (lane < m) R[(size_t)blockIdx.x * m + lane] = running;
+    return;
+  }
+
+  // ============================ counting warps ================================
+  uint32_t k = 0;
+  for (uint32_t t = t0; t < t1; ++t, ++k) {
+    const uint32_t p = k & 1u, st = k % KS;
+    if (k >= 2) mbar_wait(&cempty[p], ((k - 2) >> 1) & 1u);  // count buffer p is free again
+    uint32_t ones = 0, nvalid = SL;
+    uint32_t *row = cnt + (p * W + warp) * mS;
+    if (via_tma(t)) {
+      mbar_wait(&full[st], (k / KS) & 1u);
+      const uint4 *v = reinterpret_cast<const uint4 *>(km_smem + st * T + warp * SL);
+      uint4 q[NV];
+#pragma unroll
+      for (int u = 0; u < NV; ++u) q[u] = v[lane + 32u * (uint32_t)u];
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t b = bucket_of<KIND>(k4[e], bp);
+          if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
+        }
+      }
+    } else {  // ragged last tile / unaligned input
+      const uint64_t lo = (uint64_t)t * T + warp * SL;
+      const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
+      nvalid = hi > lo ? hi - (uint32_t)lo : 0u;
+      for (uint32_t i = (uint32_t)lo + lane; i < hi; i += 32u) {
+        const uint32_t b = bucket_of<KIND>(__ldg(keys + i), bp);
+        if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
+      }
+    }
+    if constexpr (SMALLM) {
+      ones = __reduce_add_sync(0xFFFFFFFFu, ones);
+      if (lane == 0) {
+        row[0] = nvalid - ones;
+        row[1] = ones;
+      }
+    }
+    mbar_arrive(&cfull[p]);
+  }
 }
 
 // Shared memory of kf_meta: 3 stages of [keys OS | values OS | meta MS] words,
