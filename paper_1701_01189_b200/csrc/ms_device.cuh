@@ -172,6 +172,11 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gmem_src
       : "memory");
 }
 
+// bulk prefetch global -> L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void prefetch_l2_bulk(const void *gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
+
 // 1-D bulk copy shared -> global (TMA store, SASS UBLKCP).  Addresses and size
 // must be multiples of 16 bytes; completion is tracked with bulk groups.
 __device__ __forceinline__ void tma_store_1d(void *gmem_dst, const void *smem_src, uint32_t bytes) {

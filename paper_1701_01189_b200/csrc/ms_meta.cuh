@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t kStages = 3;
+  constexpr uint32_t kPrefetchAhead = 2;  // L2 prefetch distance beyond a TMA issue
   extern __shared__ __align__(128) uint8_t kf_smem[];
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ __align__(8) uint64_t placed[kStages];  // PROD: tile placed, 512 arrivals
@@ -255,9 +256,19 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       tma_load_1d(stage0 + st * SW + MO, a.meta + (size_t)t * MS, MS * 4u, &bar[st],
                   policy_evict_first());
   };
+  // the TMA ring holds only three tiles; tiles further ahead are prefetched
+  // into L2 so that their TMA loads later see L2 latency, not DRAM latency
+  auto prefetch = [&](uint32_t t) {
+    if (tid == kProducer && t < t1 && via_tma(t)) {
+      prefetch_l2_bulk(a.keys_in + (size_t)t * T, T * 4u);
+      if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)t * T, T * 4u);
+      prefetch_l2_bulk(a.meta + (size_t)t * MS, MS * 4u);
+    }
+  };
   auto issue = [&](uint32_t t, uint32_t st) {
     issue_data(t, st);
     issue_meta(t, st);
+    prefetch(t + kPrefetchAhead);
   };
   if (tid == 0) {
     for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
@@ -273,6 +284,8 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       griddep_wait();  // meta records are complete
       issue_meta(t0, 0);
       issue_meta(t0 + 1, 1);
+      prefetch(t0 + 2);
+      prefetch(t0 + 3);
       uint32_t k = 0;
       for (uint32_t t = t0; t < t1; ++t, ++k) {
         const uint32_t st = k % kStages;
@@ -359,6 +372,8 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   griddep_wait();  // KM complete: meta records and range histograms
   issue_meta(t0, 0);
   issue_meta(t0 + 1, 1);
+  prefetch(t0 + 2);
+  prefetch(t0 + 3);
   uint32_t gbase = 0, grun = 0;
   {
     uint32_t *red = s_mask;  // [2][16][32] scratch (the mask rows are zeroed per tile)
