@@ -18,13 +18,13 @@ inline int meta_rank_mode(uint32_t m) {
   static const int forced = [] {
     const char *e = std::getenv("MS_META_RANK");
     if (!e) return -1;
-    const char *names[] = {"atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2"};
-    for (int i = 0; i < 7; ++i)
+    const char *names[] = {"atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2", "xpair"};
+    for (int i = 0; i < 8; ++i)
       if (!std::strcmp(e, names[i])) return i;
     return -1;
   }();
   if (forced >= 0) return forced;
-  return m <= 8 ? 6 : (m <= 16 ? 5 : 4);
+  return m <= 8 ? 6 : (m <= 16 ? 5 : 7);
 }
 
 template <int KIND>
@@ -194,6 +194,7 @@ cudaError_t Launch<KIND>::fused_meta(bool pairs, const KfArgs &a, const BucketPa
     MS_KFM_CASE(4);
     MS_KFM_CASE(5);
     MS_KFM_CASE(6);
+    MS_KFM_CASE(7);
     default: return pairs ? kfm_go<KIND, true, false, 2>(a, bp, grid, s) : kfm_go<KIND, false, false, 2>(a, bp, grid, s);
   }
 #undef MS_KFM_CASE

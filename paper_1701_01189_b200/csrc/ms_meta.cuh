@@ -209,7 +209,8 @@ __host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
 //               2 / 3 = ballots for every third / every second window, atomics
 //                   for the others (balances the shared-memory and ALU pipes);
 //               4 / 5 / 6 = as 0 / 2 / 3 with the atomic windows' masks taken
-//                   and cleared by one atomic exchange per bucket lane.
+//                   and cleared by one atomic exchange per bucket lane;
+//               7 = as 4, two windows in flight at a time (full tiles).
 template <int KIND, bool PAIRS, bool SMALLM, int ITEMS, int RANK, bool PROD>
 __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(KfArgs a, BucketParams bp) {
   constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
@@ -457,6 +458,36 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     bool derr = false;
     auto place = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
+      if constexpr (RANK == 7 && FULL && !SMALLM && (ITEMS % 2 == 0)) {
+        // two windows at a time: both windows' shared-memory round trips
+        // (OR of the lane bit, exchange of the bucket lane's mask) are in
+        // flight together; only the cheap running-slot update is serial
+#pragma unroll
+        for (int i = 0; i < ITEMS; i += 2) {
+          const uint32_t b0 = bucket_of<KIND>(key[i], bp), b1 = bucket_of<KIND>(key[i + 1], bp);
+          if constexpr (KIND == kIdentity)
+            derr |= key_domain_error<KIND>(key[i], bp) || key_domain_error<KIND>(key[i + 1], bp);
+          atomicOr(mrow0 + b0, lanebit);
+          atomicOr(mrow1 + b1, lanebit);
+          __syncwarp();
+          const uint32_t mine0 = atomicExch(mrow0 + lane, 0u);
+          const uint32_t mine1 = atomicExch(mrow1 + lane, 0u);
+          const uint32_t peers0 = __shfl_sync(0xFFFFFFFFu, mine0, b0);
+          const uint32_t peers1 = __shfl_sync(0xFFFFFFFFu, mine1, b1);
+          const uint32_t w1 = wrun + __popc(mine0);
+          const uint32_t slot0 = __shfl_sync(0xFFFFFFFFu, wrun, b0) + __popc(peers0 & lt);
+          const uint32_t slot1 = __shfl_sync(0xFFFFFFFFu, w1, b1) + __popc(peers1 & lt);
+          wrun = w1 + __popc(mine1);
+          __syncwarp();  // both rows are clear before the next pair's ORs
+          s_stage[slot0] = key[i];
+          s_stage[slot1] = key[i + 1];
+          if constexpr (PAIRS) {
+            s_stage[OS + slot0] = val[i];
+            s_stage[OS + slot1] = val[i + 1];
+          }
+        }
+        return;
+      }
       uint32_t base0 = 0, base1 = 0, c0 = 0, c1 = 0;
       if constexpr (SMALLM) {
         base0 = __shfl_sync(0xFFFFFFFFu, wrun, 0);
@@ -509,7 +540,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
           // bucket j's mask and clears it with one atomic exchange, the key of
           // bucket b gets its peers and running slot from lane b by shuffles.
           // Two rows alternate over the atomic windows, one __syncwarp each.
-          const int r = RANK == 4 ? (i & 1) : (RANK == 5 ? (i % 3) : ((i >> 1) & 1));
+          const int r = (RANK == 4 || RANK == 7) ? (i & 1) : (RANK == 5 ? (i % 3) : ((i >> 1) & 1));
           uint32_t *mrow = r ? mrow1 : mrow0;
           if (valid) atomicOr(mrow + b, lanebit);
           __syncwarp();
