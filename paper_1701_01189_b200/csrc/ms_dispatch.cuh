@@ -18,8 +18,8 @@ inline int meta_rank_mode(uint32_t m) {
   static const int forced = [] {
     const char *e = std::getenv("MS_META_RANK");
     if (!e) return -1;
-    const char *names[] = {"atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2", "xpair"};
-    for (int i = 0; i < 8; ++i)
+    const char *names[] = {"atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2", "xpair", "inc"};
+    for (int i = 0; i < 9; ++i)
       if (!std::strcmp(e, names[i])) return i;
     return -1;
   }();
@@ -195,6 +195,7 @@ cudaError_t Launch<KIND>::fused_meta(bool pairs, const KfArgs &a, const BucketPa
     MS_KFM_CASE(5);
     MS_KFM_CASE(6);
     MS_KFM_CASE(7);
+    MS_KFM_CASE(8);
     default: return pairs ? kfm_go<KIND, true, false, 2>(a, bp, grid, s) : kfm_go<KIND, false, false, 2>(a, bp, grid, s);
   }
 #undef MS_KFM_CASE

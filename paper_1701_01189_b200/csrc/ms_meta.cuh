@@ -458,6 +458,28 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     bool derr = false;
     auto place = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
+      if constexpr (RANK == 8 && !SMALLM) {
+        // rank by the shared-memory atomic increment of this warp's running
+        // slot of the bucket: relies on same-address increments of one warp
+        // instruction being returned in lane order (checked bit-exactly by
+        // the parity tests; MS_META_RANK selects the other modes)
+        uint32_t *brow = mrow0;
+        if (lane < m) brow[lane] = wrun;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const bool valid = FULL || wbase + (uint32_t)i * 32u + lane < tn;
+          if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;
+          const uint32_t b = bucket_of<KIND>(key[i], bp);
+          if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+          if (valid) {
+            const uint32_t slot = atomicAdd(brow + b, 1u);
+            s_stage[slot] = key[i];
+            if constexpr (PAIRS) s_stage[OS + slot] = val[i];
+          }
+        }
+        return;
+      }
       if constexpr (RANK == 7 && FULL && !SMALLM && (ITEMS % 2 == 0)) {
         // two windows at a time: both windows' shared-memory round trips
         // (OR of the lane bit, exchange of the bucket lane's mask) are in
