@@ -36,6 +36,7 @@ _U32P = ctypes.POINTER(ctypes.c_uint32)
 SIGNATURES = [
     ("ms_status_string", ctypes.c_char_p, [_I]),
     ("ms_version", ctypes.c_char_p, []),
+    ("ms_lane_ordered_increment", _I, []),
     ("ms_bucket_delta_default", _I, [_U32, _FN]),
     ("ms_bucket_identity", _I, [_U32, _FN]),
     ("ms_bucket_radix", _I, [_U32, _U32, _FN]),

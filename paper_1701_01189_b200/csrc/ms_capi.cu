@@ -13,6 +13,27 @@
 
 using namespace ms;
 
+namespace ms {
+// RANK 8 probe (see k_probe_lane_ordered_inc): runs once, synchronously, on a
+// private stream at the first m <= 32 multisplit of the process.
+bool lane_ordered_inc() {
+  static const bool ok = [] {
+    uint32_t *d = nullptr, h = 0;
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return false;
+    bool r = false;
+    if (cudaMallocAsync((void **)&d, 4, st) == cudaSuccess) {
+      k_probe_lane_ordered_inc<<<1, 32, 0, st>>>(d);
+      r = cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+          cudaFreeAsync(d, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess && h == 1u;
+    }
+    cudaStreamDestroy(st);
+    return r;
+  }();
+  return ok;
+}
+}  // namespace ms
+
 namespace {
 
 thread_local void *const *g_stage_events = nullptr;
@@ -412,6 +433,8 @@ const char *ms_status_string(ms_status s) {
 
 const char *ms_version(void) { return "0.1.0"; }
 
+int ms_lane_ordered_increment(void) { return ms::lane_ordered_inc() ? 1 : 0; }
+
 ms_status ms_bucket_delta_default(uint32_t m, ms_bucket_fn *out) {
   if (!out) return MS_ERR_INVALID_VALUE;
   if (m < 1 || m > 256) return MS_ERR_UNSUPPORTED;
@@ -437,6 +460,7 @@ ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out) {
 ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn); }
 
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
+  if (m >= 3 && m <= 32 && n > 0) (void)ms::lane_ordered_inc();  // probe outside any capture
   if (m < 1) m = 1;
   if (m > 256) m = 256;
   return layout_for(n, m, with_values != 0).total;

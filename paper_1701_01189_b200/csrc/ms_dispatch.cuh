@@ -11,6 +11,10 @@
 namespace ms {
 
 // MS_META_RANK=atomic selects the shared-memory atomicOr peer masks in kf_meta
+// Whether this GPU returns same-address shared-memory increments in lane order
+// (RANK 8); probed once per process on a private stream (ms_capi.cu).
+bool lane_ordered_inc();
+
 // kf_meta's RANK for m buckets: MS_META_RANK = atomic | ballot | mix3 | mix2 |
 // xatomic | xmix3 | xmix2 overrides; by default the choice measured best per
 // number of bucket bits (profiles/r01/s2_rank_modes.md)
@@ -24,6 +28,7 @@ inline int meta_rank_mode(uint32_t m) {
     return -1;
   }();
   if (forced >= 0) return forced;
+  if (lane_ordered_inc()) return 8;
   return m <= 8 ? 6 : (m <= 16 ? 5 : 7);
 }
 

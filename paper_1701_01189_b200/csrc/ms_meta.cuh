@@ -179,6 +179,34 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
   }
 }
 
+// ============================================================================
+// Probe for kf_meta's RANK 8: one warp checks, over many bucket patterns, that
+// the values a shared-memory atomicAdd(p, 1) instruction returns to the lanes
+// that share an address are consecutive in lane order (what a stable rank
+// needs).  flag[0] = 1 if every pattern held.
+// ============================================================================
+static __global__ void __launch_bounds__(32) k_probe_lane_ordered_inc(uint32_t *flag) {
+  __shared__ uint32_t ctr[32];
+  const uint32_t lane = threadIdx.x & 31u, lt = lanemask_lt();
+  bool ok = true;
+  for (uint32_t pat = 0; pat < 4096; ++pat) {
+    ctr[lane] = pat;  // arbitrary starting values
+    __syncwarp();
+    uint32_t h = (pat * 0x9E3779B9u) ^ (lane * 0x85EBCA6Bu);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    const uint32_t mb = 1u + (pat & 31u);  // buckets in play: 1 .. 32
+    const uint32_t b = (pat & 64u) ? (lane * mb) >> 5 : h % mb;  // runs or random
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+    const uint32_t got = atomicAdd(ctr + b, 1u);
+    ok &= got == pat + (uint32_t)__popc(peers & lt);
+    __syncwarp();
+  }
+  ok = __all_sync(0xFFFFFFFFu, ok);
+  if (lane == 0) flag[0] = ok ? 1u : 0u;
+}
+
 // Shared memory of kf_meta: 3 stages of [keys OS | values OS | meta MS] words,
 // peer masks [3][W][32], run tables [2][3][32] (or deltas [2][32]).
 __host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
