@@ -306,7 +306,11 @@ def run_ours(args, rank, world, local_rank):
     if stages is not None:
         ks_bytes = n * (16 if wl["pairs"] else 8)
         achieved = ks_bytes / (stages["postscan"] * 1e-3) / 1e9
-        roofline = {"kernel": "kf_fused (KF: rank + reorder + scatter)", "bound": "hbm", "achieved": round(achieved, 1),
+        # m <= 32: KM (prescan + per-(tile, warp) slot bases) -> KF kf_meta; otherwise
+        # KU -> KR -> KF kf_fused
+        kname = ("kf_meta (KF: rank + in-place reorder + run stores)" if m <= 32 and wl["kind"] != "sort"
+                 else "kf_fused (KF: count + scan + rank + reorder + scatter)")
+        roofline = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1),
                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                     "traffic": load_traffic(f"{args.workload}_m{m}"),
                     "alg_bytes_per_launch": ks_bytes, "peak_source": peak_src,

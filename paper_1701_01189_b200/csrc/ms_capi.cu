@@ -294,6 +294,14 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.store_runs = m <= 64 && lo.T / m >= 256u && (((uintptr_t)keys_out & 15u) == 0) &&
                  (!pairs || (((uintptr_t)vals_out & 15u) == 0)) && !env_flag("MS_NO_RUN_STORES");
 
+  {
+    static const uint32_t pf = [] {
+      const char *v = std::getenv("MS_KF_PREFETCH");
+      return v ? (uint32_t)std::atoi(v) : 2u;
+    }();
+    a.prefetch_ahead = pf;
+  }
+
   if (n <= lo.T) {  // one subproblem: a single launch
     a.mode = kModeSingle;
     a.num_tiles = 1;

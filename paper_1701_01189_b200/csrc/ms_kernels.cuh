@@ -242,6 +242,7 @@ struct KfArgs {
   int mode;
   int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
+  uint32_t prefetch_ahead;  // kf_meta: L2 bulk prefetch distance (tiles) beyond each TMA load
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),

@@ -244,7 +244,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t kStages = 3;
-  constexpr uint32_t kPrefetchAhead = 2;  // L2 prefetch distance beyond a TMA issue
   extern __shared__ __align__(128) uint8_t kf_smem[];
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ __align__(8) uint64_t placed[kStages];  // PROD: tile placed, 512 arrivals
@@ -297,7 +296,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   auto issue = [&](uint32_t t, uint32_t st) {
     issue_data(t, st);
     issue_meta(t, st);
-    prefetch(t + kPrefetchAhead);
+    prefetch(t + a.prefetch_ahead);
   };
   if (tid == 0) {
     for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
@@ -313,8 +312,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       griddep_wait();  // meta records are complete
       issue_meta(t0, 0);
       issue_meta(t0 + 1, 1);
-      prefetch(t0 + 2);
-      prefetch(t0 + 3);
+      for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(t0 + j);
       uint32_t k = 0;
       for (uint32_t t = t0; t < t1; ++t, ++k) {
         const uint32_t st = k % kStages;
@@ -401,18 +399,26 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   griddep_wait();  // KM complete: meta records and range histograms
   issue_meta(t0, 0);
   issue_meta(t0 + 1, 1);
-  prefetch(t0 + 2);
-  prefetch(t0 + 3);
+  for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(t0 + j);
   uint32_t gbase = 0, grun = 0;
   {
     uint32_t *red = s_mask;  // [2][16][32] scratch (the mask rows are zeroed per tile)
     const uint32_t G = a.num_ranges, c = blockIdx.x;
     uint32_t pre = 0, tot = 0;
     if (lane < m) {
-      for (uint32_t r = warp; r < G; r += W) {
-        const uint32_t v = __ldg(a.R + (size_t)r * m + lane);
-        tot += v;
-        pre += r < c ? v : 0u;
+      // batches of 8 independent loads (rows warp, warp + W, ...)
+      for (uint32_t r0 = warp; r0 < G; r0 += 8 * W) {
+        uint32_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t r = r0 + j * W;
+          v[j] = r < G ? __ldg(a.R + (size_t)r * m + lane) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          tot += v[j];
+          pre += r0 + j * W < c ? v[j] : 0u;
+        }
       }
     }
     red[warp * 32 + lane] = pre;
