@@ -63,12 +63,12 @@ const char *ms_status_string(ms_status s);
 const char *ms_version(void);
 
 /* 1 if the current GPU returns the old values of one warp instruction's
- * same-address shared-memory increments in lane order, else 0.  For m <= 32
+ * same-address shared-memory increments in lane order, else 0.  For m >= 3
  * the postscan ranks a window's keys with such increments of the warp's
  * running slot per bucket (Eq.4 term 1); stability needs the lane
  * order, so the library probes it once per process (one 32-thread kernel on a
  * private stream, synchronous) and otherwise ranks with peer masks.  Called
- * implicitly by ms_multisplit_workspace_size() and the first m <= 32 call;
+ * implicitly by ms_multisplit_workspace_size() and the first m >= 3 call;
  * call it (or the workspace query) before capturing a CUDA graph.  Errors:
  * any CUDA failure of the probe reads as 0. */
 int ms_lane_ordered_increment(void);

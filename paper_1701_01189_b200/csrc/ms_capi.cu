@@ -300,6 +300,8 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
       return v ? (uint32_t)std::atoi(v) : 2u;
     }();
     a.prefetch_ahead = pf;
+    static const bool inc_off = env_flag("MS_NO_RANK_INC");
+    a.rank_inc = m > 2 && !inc_off && ms::lane_ordered_inc();
   }
 
   if (n <= lo.T) {  // one subproblem: a single launch
@@ -468,7 +470,7 @@ ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out) {
 ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn); }
 
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
-  if (m >= 3 && m <= 32 && n > 0) (void)ms::lane_ordered_inc();  // probe outside any capture
+  if (m >= 3 && n > 0) (void)ms::lane_ordered_inc();  // probe outside any capture
   if (m < 1) m = 1;
   if (m > 256) m = 256;
   return layout_for(n, m, with_values != 0).total;

@@ -242,7 +242,8 @@ struct KfArgs {
   int mode;
   int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
-  uint32_t prefetch_ahead;  // kf_meta: L2 bulk prefetch distance (tiles) beyond each TMA load
+  uint32_t prefetch_ahead;  // L2 bulk prefetch distance (tiles) beyond each TMA load
+  int rank_inc;    // rank by lane-ordered shared-memory increments (ms_lane_ordered_increment)
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),
@@ -317,11 +318,15 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   // ---- 1. count pass: each warp's bucket counts (Eq.4 terms 2-3 need them
   //         before any element can be placed) -----------------------------------
   if constexpr (!SMALLM) {
-    for (uint32_t j = lane; j < m; j += 32) {
-      mrow0[j] = 0u;
-      mrow1[j] = 0u;
-      if constexpr (SCAN == 1) mrow2[j] = 0u;
-      crow[j] = 0u;
+    if (a.rank_inc) {
+      for (uint32_t j = lane; j < m; j += 32) crow[j] = 0u;
+    } else {
+      for (uint32_t j = lane; j < m; j += 32) {
+        mrow0[j] = 0u;
+        mrow1[j] = 0u;
+        if constexpr (SCAN == 1) mrow2[j] = 0u;
+        crow[j] = 0u;
+      }
     }
     __syncwarp();
   }
@@ -504,6 +509,20 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
   }  // block scan
 
 
+  // ---- 3'. rank and place by lane-ordered increments of this warp's running
+  //          slot per bucket (one shared-memory atomic per key; m > 2)
+  if (!SMALLM && a.rank_inc) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = valid_at(i);
+      if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;
+      if (valid) {
+        const uint32_t slot = atomicAdd(brow + bucket_of<KIND>(key[i], bp), 1u);
+        out_k[slot] = key[i];
+        if constexpr (PAIRS) out_v[slot] = val[i];
+      }
+    }
+  } else
   // ---- 3. rank and place, window by window (Eq.4 term 1 + the running slot) --
   // Peer masks come from one shared-memory OR of the lane bit per key (the
   // ballot-based voting of Alg.3, in one instruction); masks are
@@ -672,6 +691,12 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
       tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
       if constexpr (PAIRS) tma_load_1d(dst + OS, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
+      // tiles beyond the three-stage ring: into L2 ahead of their TMA loads
+      const uint32_t tp = t + a.prefetch_ahead;
+      if (a.mode == kModeRange && a.prefetch_ahead && tp < t1 && tile_n(tp) == T) {
+        prefetch_l2_bulk(a.keys_in + (size_t)tp * T, T * 4u);
+        if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)tp * T, T * 4u);
+      }
     }
   };
   if (tid == 0) {
