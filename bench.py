@@ -51,6 +51,16 @@ WORKLOADS = {
                       desc="multisplit LSD radix sort, 2^28 uint32 keys, 4 x 8-bit (configs[3])"),
     "sort_pairs": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80,
                        desc="multisplit LSD radix sort, 2^28 pairs, 4 x 8-bit (configs[3])"),
+    # the same sorts with 5-bit digits: 7 passes through the m <= 32 pipeline
+    # (the paper's Table 8 sweeps r); bpe counts the 7 passes
+    "sort_keys_r5": dict(n=1 << 28, pairs=False, kind="sort", m=32, bits=5, unit="Gkeys/s", bpe=84,
+                         desc="multisplit LSD radix sort, 2^28 uint32 keys, 6 x 5-bit + 1 x 2-bit"),
+    "sort_pairs_r5": dict(n=1 << 28, pairs=True, kind="sort", m=32, bits=5, unit="Gpairs/s", bpe=140,
+                          desc="multisplit LSD radix sort, 2^28 pairs, 6 x 5-bit + 1 x 2-bit"),
+    "sort_keys_r4": dict(n=1 << 28, pairs=False, kind="sort", m=16, bits=4, unit="Gkeys/s", bpe=96,
+                         desc="multisplit LSD radix sort, 2^28 uint32 keys, 8 x 4-bit"),
+    "sort_pairs_r4": dict(n=1 << 28, pairs=True, kind="sort", m=16, bits=4, unit="Gpairs/s", bpe=160,
+                          desc="multisplit LSD radix sort, 2^28 pairs, 8 x 4-bit"),
 }
 SEED = 0x5EED
 
@@ -176,7 +186,8 @@ class Runner:
             self.ko, self.vo, _ = sharded.sharded_multisplit(keys, self.vals, self.bucket)
             return
         if self.bucket is None:
-            self.ms.radix_sort(keys, self.vals, out_keys=ko, out_values=self.vo, workspace=self.ws)
+            self.ms.radix_sort(keys, self.vals, bits_per_pass=self.wl.get("bits", 8), out_keys=ko,
+                               out_values=self.vo, workspace=self.ws)
         else:
             self.ms.multisplit(keys, self.vals, bucket=self.bucket, out_keys=ko, out_values=self.vo,
                                out_offsets=self.off, workspace=self.ws)
@@ -350,7 +361,7 @@ def sweep(args, dev, flush, hbm):
     res = {}
     cases = [("ms_keys", m) for m in (2, 8, 32, 64, 256)] + [("ms_pairs", m) for m in (2, 8, 32, 256)] + \
             [("ms_pairs_c3", 64), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256), ("sort_keys", 256),
-             ("sort_pairs", 256)]
+             ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32)]
     for name, m in cases:
         wl = WORKLOADS[name]
         run = Runner(wl, m, dev)

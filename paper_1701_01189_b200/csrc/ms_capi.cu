@@ -301,7 +301,9 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
     }();
     a.prefetch_ahead = pf;
     static const bool inc_off = env_flag("MS_NO_RANK_INC");
-    a.rank_inc = m > 2 && !inc_off && ms::lane_ordered_inc();
+    // measured (profiles/r01/s2_summary.md): increments win for keys and for
+    // m <= 32; peer masks for pairs with m > 32
+    a.rank_inc = m > 2 && (!pairs || m <= 32) && !inc_off && ms::lane_ordered_inc();
   }
 
   if (n <= lo.T) {  // one subproblem: a single launch

@@ -247,16 +247,19 @@ struct KfArgs {
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),
-// chosen so that two (m <= 32) or three (m > 32) CTAs fit in an SM's 228 KB:
-//   class 0, m <= 32 : keys 16 x 16 (T 8192), pairs 16 x 8 (T 4096), warp scan, 1 bucket/lane
-//   class 1, m <= 64 : keys  8 x 16 (T 4096), pairs  8 x 8 (T 2048), warp scan, 2 buckets/lane
-//   class 2, m >  64 : keys  8 x 16 (T 4096), pairs  8 x 8 (T 2048), block scan
+// chosen so that two (m <= 32, pairs) or three (keys, m > 32) CTAs fit in an SM's 228 KB:
+//   class 0, m <= 32 : keys 16 x 16 (T 8192), pairs 16 x 16 (T 4096), warp scan, 1 bucket/lane
+//   class 1, m <= 64 : keys  8 x 16 (T 4096), pairs  8 x 16 (T 4096), warp scan, 2 buckets/lane
+//   class 2, m >  64 : keys  8 x 16 (T 4096), pairs  8 x 16 (T 4096), block scan
+// (pairs: 4096-pair tiles measured faster than 2048 at m = 256: bucket runs of
+// 16 instead of 8 elements, fewer partially written sectors)
 __host__ __device__ constexpr int kf_class(uint32_t m) { return m <= 32 ? 0 : (m <= 64 ? 1 : 2); }
 struct KfShape {
   int warps, items, ctas_per_sm;
 };
 __host__ __device__ constexpr KfShape kf_shape(bool pairs, int cls) {
-  return cls == 0 ? KfShape{16, pairs ? 8 : 16, 2} : KfShape{8, pairs ? 8 : 16, 3};
+  // classes 1-2, pairs: 4096-pair tiles (bucket runs of 16 at m = 256), 2 CTAs / SM
+  return cls == 0 ? KfShape{16, pairs ? 8 : 16, 2} : (pairs ? KfShape{8, 16, 2} : KfShape{8, 16, 3});
 }
 __host__ __device__ constexpr uint32_t kf_tile(bool pairs, int cls) {
   return 32u * (uint32_t)kf_shape(pairs, cls).warps * (uint32_t)kf_shape(pairs, cls).items;
@@ -272,12 +275,14 @@ __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
 // | peer masks [2 or 3][W][m]
 // | per-warp counts [W][m] | per-warp running slots [W][m] (m <= 64) | delta[m]
 // | run table [3][m] (m <= 64)
-__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs) {
+// (inc: ranking by lane-ordered increments, no peer-mask rows)
+__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs, bool inc = false) {
   const int cls = kf_class(m);
   const size_t T = kf_tile(pairs, cls), W = (size_t)kf_shape(pairs, cls).warps;
   const size_t k = pairs ? 2u : 1u;
   const size_t mm = m < 2 ? 2 : m;
-  const size_t rows = cls == 2 ? 3 : (cls == 1 ? 4 : 5);  // masks (2 or 3) + counts (+ slots)
+  const size_t mrows = inc ? 0 : (cls == 0 ? 3 : 2);
+  const size_t rows = mrows + (cls == 2 ? 1 : 2);  // masks + counts (+ slots)
   const size_t tables = cls == 2 ? 1 : 4;
   return 3 * (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 + tables * mm * 4;
 }
@@ -670,7 +675,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kf_smem);
   uint32_t *s_mask = stage0 + kStages * SW;
   constexpr uint32_t kMaskRows = SCAN == 1 ? 3 : 2;  // m <= 32: triple-buffered masks
-  uint32_t *s_cnt = s_mask + kMaskRows * W * mm;
+  uint32_t *s_cnt = s_mask + (a.rank_inc ? 0u : kMaskRows) * W * mm;  // no masks when ranking by increments
   uint32_t *s_base = s_cnt + W * mm;  // WSCAN only
   uint32_t *s_delta = WSCAN ? s_base + W * mm : s_base;
   uint32_t *s_run = s_delta + mm;

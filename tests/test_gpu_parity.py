@@ -79,7 +79,7 @@ T = 8192  # ms.tile_size() for keys (4096 for pairs); checked below
 
 def test_tile_size():
     assert [ms.tile_size(m, p) for m in (2, 32, 33, 64, 65, 256) for p in (False, True)] == \
-        [T, T // 2, T, T // 2, T // 2, T // 4, T // 2, T // 4, T // 2, T // 4, T // 2, T // 4]
+        [T, T // 2, T, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2]
 
 
 @pytest.mark.parametrize("n", [T - 1, T, T + 1, 2 * T - 3, 3 * T + 5, 37 * T + 4097])
