@@ -124,10 +124,11 @@ def device_status(workspace: torch.Tensor | None = None, stream=None) -> int:
 
 
 def radix_sort(keys: torch.Tensor, values: torch.Tensor | None = None, *, begin_bit: int = 0,
-               end_bit: int = 32, bits_per_pass: int = 8, out_keys: torch.Tensor | None = None,
+               end_bit: int = 32, bits_per_pass: int = 0, out_keys: torch.Tensor | None = None,
                out_values: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                stream=None):
-    """LSD multisplit radix sort (Sec.7.1): stable sort by key bits [begin_bit, end_bit)."""
+    """LSD multisplit radix sort (Sec.7.1): stable sort by key bits [begin_bit, end_bit).
+    bits_per_pass = 0: the library's choice (5-bit digits, see include/multisplit.h)."""
     lib = _lib.load()
     keys = _u32view(keys, "keys")
     n = keys.numel()

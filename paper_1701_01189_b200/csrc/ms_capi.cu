@@ -495,6 +495,7 @@ ms_status ms_multisplit_pairs(const uint32_t *keys_in, const uint32_t *vals_in,
 
 int ms_radix_pass_schedule(uint32_t begin_bit, uint32_t end_bit, uint32_t r, uint32_t *shifts,
                            uint32_t *bits, int cap) {
+  if (r == 0) r = 5;  // library choice: digits that use the m <= 32 pipeline
   if (r < 1 || r > 8 || begin_bit >= end_bit || end_bit > 32) return -1;
   int p = 0;
   for (uint32_t s = begin_bit; s < end_bit; s += r, ++p) {
