@@ -382,6 +382,13 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.Tot = base;
   a.tiles_per_cta = K;
   a.num_ranges = G;
+  {
+    // per-element scatter holding back partial trailing sectors: correct but
+    // measured 1.1-1.8x slower, so opt-in via MS_CARRY=1
+    static const bool carry_env = env_flag("MS_CARRY");
+    a.carry = carry_env && m > 32 && !a.store_runs;
+    a.carry_m = m;
+  }
   const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;

@@ -99,7 +99,7 @@ static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid,
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kf_smem_bytes(CLS == 0 ? 32 : (CLS == 1 ? 64 : kMaxBuckets), PAIRS));
+                                         (int)kf_smem_bytes(CLS == 0 ? 32 : (CLS == 1 ? 64 : kMaxBuckets), PAIRS, false, true));
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -108,7 +108,7 @@ static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid,
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(sh.warps * 32);
-  cfg.dynamicSmemBytes = kf_smem_bytes(bp.m, PAIRS, a.rank_inc != 0);
+  cfg.dynamicSmemBytes = kf_smem_bytes(bp.m, PAIRS, a.rank_inc != 0, a.carry != 0);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
