@@ -133,3 +133,33 @@ def values(n: int, seed: int, parity: bool = True) -> np.ndarray:
         idx = np.arange(s, min(n, s + _CHUNK), dtype=np.uint64)
         out[s:s + idx.size] = rnd32(seed, 8, idx)
     return out
+
+
+def floats(n: int, seed: int, upper: float = 1024.0) -> np.ndarray:
+    """Histogram samples U[0, upper) (Sec.7.3: 2^25 floats in [0, 1024)):
+    x_i = (rnd32(seed, 10, i) >> 8) * upper * 2^-24, exact in binary32 when upper
+    is a power of two."""
+    out = np.empty(n, np.float32)
+    scale = np.float64(upper) / float(1 << 24)
+    for s in range(0, n, _CHUNK):
+        idx = np.arange(s, min(n, s + _CHUNK), dtype=np.uint64)
+        r = (rnd32(seed, 10, idx) >> np.uint32(8)).astype(np.float64)
+        out[s:s + idx.size] = (r * scale).astype(np.float32)
+    return out
+
+
+def splitters(m: int, seed: int, upper: float = 1024.0) -> np.ndarray:
+    """Range-histogram splitters s_0 = 0 < s_1 < ... < s_m = upper: m-1 distinct
+    random interior values on the same 2^-24 * upper grid."""
+    got: list[float] = []
+    seen = set()
+    i = 0
+    scale = upper / float(1 << 24)
+    while len(got) < m - 1:
+        r = int(rnd32(seed, 11, np.array([i], np.uint64))[0]) >> 8
+        i += 1
+        if r == 0 or r in seen:
+            continue
+        seen.add(r)
+        got.append(r * scale)
+    return np.array([0.0] + sorted(got) + [upper], dtype=np.float32)

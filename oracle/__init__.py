@@ -39,7 +39,8 @@ def build(force: bool = False) -> str:
     """Compile the oracle C file into ``oracle/liborc.so`` (gcc, -O2)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-shared", "-fPIC",
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -60,8 +61,12 @@ def _load():
         lib.orc_global_scan.argtypes = [p, u64, u32, p]
         lib.orc_global_scan.restype = None
         lib.orc_radix_sort.argtypes = [p, p, p, p, u64, u32, u32]
+        f32 = ctypes.c_float
+        lib.orc_histogram_even.argtypes = [p, u64, u32, f32, f32, p]
+        lib.orc_histogram_range.argtypes = [p, u64, u32, p, p]
         for f in (lib.orc_validate, lib.orc_bucket, lib.orc_multisplit,
-                  lib.orc_tile_histogram, lib.orc_radix_sort):
+                  lib.orc_tile_histogram, lib.orc_radix_sort, lib.orc_histogram_even,
+                  lib.orc_histogram_range):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -163,3 +168,33 @@ def radix_sort(keys, values=None, begin_bit: int = 0, end_bit: int = 32):
     if st:
         raise OracleError(st)
     return ko, vo
+
+
+def _f32(a) -> np.ndarray:
+    a = np.ascontiguousarray(a)
+    if a.dtype != np.float32:
+        a = a.astype(np.float32)
+    return a
+
+
+def histogram_even(samples, m: int, lower: float, upper: float) -> np.ndarray:
+    """Even histogram (Sec.7.3): counts[m] of floor((x - s_0) / Delta)."""
+    x = _f32(samples)
+    c = np.empty(max(m, 1), np.uint32)
+    st = _load().orc_histogram_even(_ptr(x), x.size, m, float(np.float32(lower)),
+                                    float(np.float32(upper)), _ptr(c))
+    if st:
+        raise OracleError(st)
+    return c
+
+
+def histogram_range(samples, splitters) -> np.ndarray:
+    """Range histogram (Sec.7.3): counts[m] by upper-bound over m+1 splitters."""
+    x = _f32(samples)
+    s = _f32(splitters)
+    m = s.size - 1
+    c = np.empty(max(m, 1), np.uint32)
+    st = _load().orc_histogram_range(_ptr(x), x.size, m, _ptr(s), _ptr(c))
+    if st:
+        raise OracleError(st)
+    return c

@@ -27,12 +27,25 @@
  *   orc_global_scan     G = exclusive scan of row-vectorized H (P:291, P:777,
  *                       Alg.1 P:804-812 with the index typo read as i*L+j,
  *                       reading R3), returned in the same tile-major storage.
+ *   orc_histogram_even  device-wide histogram, Even scenario (Sec.7.3,
+ *                       P:1890): m buckets of width Delta = (s_m - s_0) / m
+ *                       between s_0 and s_m; bucket of x = floor((x - s_0) /
+ *                       Delta), all in IEEE binary32 round-to-nearest
+ *                       (reading R25); x outside [s_0, s_m) or NaN is not
+ *                       counted, a quotient of m (rounding at the top edge)
+ *                       is clamped to m-1 (reading R26).
+ *   orc_histogram_range device-wide histogram, Range scenario (Sec.7.3,
+ *                       P:1891): splitters s_0 < ... < s_m; bucket of x = the
+ *                       j with s_j <= x < s_{j+1}, found by the upper-bound
+ *                       search the paper names, written here as a linear
+ *                       count of splitters <= x (reading R26).
  *   orc_radix_sort      the result of multisplit-sort (Sec.7.1):
  *                       a stable sort of (keys,values) by the key bits
  *                       [begin_bit, end_bit) as unsigned integers, written as
  *                       a plain stable merge sort (the plain definition of
  *                       what LSD stable passes produce, reading R10).
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -188,5 +201,43 @@ int orc_radix_sort(const uint32_t *keys_in, const uint32_t *vals_in,
   }
   free(idx);
   free(tmp);
+  return ORC_OK;
+}
+
+/* ---------------------------------------------------------------- histogram
+ * Sec.7.3.  counts[0..m) are overwritten.  Returns
+ * ORC_ERR_UNSUPPORTED for m outside 1..256 (the paper's scope), ORC_ERR_INVALID
+ * for empty or unordered bounds / splitters. */
+int orc_histogram_even(const float *x, uint64_t n, uint32_t m, float lower, float upper,
+                       uint32_t *counts) {
+  if (m < 1 || m > 256) return ORC_ERR_UNSUPPORTED;
+  if (!(lower < upper)) return ORC_ERR_INVALID;
+  volatile float delta = (upper - lower) / (float)m; /* binary32, round to nearest */
+  for (uint32_t j = 0; j < m; ++j) counts[j] = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const float v = x[i];
+    if (!(v >= lower && v < upper)) continue; /* outside [s_0, s_m) or NaN */
+    volatile float d = v - lower;
+    volatile float q = d / delta;
+    uint32_t b = (uint32_t)floorf(q);
+    if (b > m - 1) b = m - 1;
+    counts[b]++;
+  }
+  return ORC_OK;
+}
+
+int orc_histogram_range(const float *x, uint64_t n, uint32_t m, const float *s,
+                        uint32_t *counts) {
+  if (m < 1 || m > 256) return ORC_ERR_UNSUPPORTED;
+  for (uint32_t j = 0; j < m; ++j)
+    if (!(s[j] < s[j + 1])) return ORC_ERR_INVALID;
+  for (uint32_t j = 0; j < m; ++j) counts[j] = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const float v = x[i];
+    if (!(v >= s[0] && v < s[m])) continue;
+    uint32_t le = 0; /* number of splitters <= v: upper_bound(s, s+m+1, v) - s */
+    for (uint32_t j = 0; j <= m; ++j) le += s[j] <= v;
+    counts[le - 1]++;
+  }
   return ORC_OK;
 }

@@ -374,3 +374,76 @@ def test_metric_definitions_sol():
         assert abs(bw / 12 - ks) < 0.1 and abs(bw / 20 - ps) < 0.1
     n = 2**25
     assert abs(n / 1.77e-3 / 1e9 - 18.93) < 0.05
+
+
+# ---------------------------------------------------------------- histogram (Sec.7.3)
+def _hist_edge_samples(s):
+    """samples on and next to every splitter, outside the range, NaN, and the grid."""
+    s = np.asarray(s, np.float32)
+    pts = [s, np.nextafter(s, np.float32(-np.inf)), np.nextafter(s, np.float32(np.inf)),
+           np.array([-1.0, -0.0, 2048.0, np.nan, np.inf, -np.inf], np.float32)]
+    return np.concatenate(pts + [gen.floats(5000, seed=4)]).astype(np.float32)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 7, 64, 255, 256])
+def test_histogram_range_is_searchsorted(m):
+    # Range scenario = upper-bound search (P:1891) = numpy.searchsorted(side="right") - 1
+    s = gen.splitters(m, seed=m)
+    x = _hist_edge_samples(s)
+    inside = (x >= s[0]) & (x < s[m])
+    b = np.searchsorted(s, x[inside], side="right") - 1
+    expect = np.bincount(b, minlength=m).astype(np.uint32)
+    assert np.array_equal(oracle.histogram_range(x, s), expect)
+
+
+@pytest.mark.parametrize("k", [0, 1, 3, 5, 8])
+def test_histogram_even_power_of_two_exact(k):
+    # Delta = 1024 / 2^k is a power of two: floor((x - 0) / Delta) is exact, so the
+    # bucket is integer arithmetic on the sample's grid value x * 2^14 (gen.floats)
+    m = 1 << k
+    x = gen.floats(20000, seed=9)
+    xi = (x.astype(np.float64) * (1 << 14)).astype(np.int64)  # exact integers
+    width = (1024 // m) * (1 << 14)
+    expect = np.bincount(xi // width, minlength=m).astype(np.uint32)
+    assert np.array_equal(oracle.histogram_even(x, m, 0.0, 1024.0), expect)
+
+
+@pytest.mark.parametrize("k", [1, 4, 8])
+def test_histogram_even_equals_range_on_even_splitters(k):
+    m = 1 << k
+    s = (np.arange(m + 1) * (1024.0 / m)).astype(np.float32)  # exact
+    x = _hist_edge_samples(s)
+    assert np.array_equal(oracle.histogram_even(x, m, 0.0, 1024.0), oracle.histogram_range(x, s))
+
+
+@pytest.mark.parametrize("m", [3, 7, 100, 255])
+def test_histogram_even_general_m_matches_exact_quotient_off_boundary(m):
+    # reading R25: binary32 quotient; away from bucket boundaries it must equal the
+    # floor of the exact rational quotient (x - s0) / fl((s_m - s0) / m)
+    from fractions import Fraction
+    lo, hi = np.float32(0.0), np.float32(1000.0)
+    delta = Fraction(float(np.float32((hi - lo) / np.float32(m))))
+    x = gen.floats(3000, seed=m) * np.float32(1000.0 / 1024.0)
+    c = oracle.histogram_even(x, m, float(lo), float(hi))
+    expect = np.zeros(m, np.int64)
+    unsure = 0
+    for v in x.astype(np.float64):
+        q = (Fraction(v) - Fraction(float(lo))) / delta
+        fl = q.numerator // q.denominator
+        if abs(q - round(q)) < Fraction(1, 10000):
+            unsure += 1
+            continue
+        expect[min(fl, m - 1)] += 1
+    assert unsure < 30
+    assert int(c.sum()) == x.size
+    assert np.all(np.abs(c.astype(np.int64) - expect) <= unsure)
+
+
+def test_histogram_worked_example():
+    # P:1890 with s_0 = 0, s_m = 1024, m = 256 (Delta = 4): 0, 0.5, 3.9 -> bucket 0;
+    # 4 -> 1; 1023.99 -> 255; 1024 (= s_m), -1 and NaN are outside [s_0, s_m) (reading R26)
+    x = np.array([0, 0.5, 3.9, 4, 1023.99, 1024, -1, np.nan], np.float32)
+    c = oracle.histogram_even(x, 256, 0.0, 1024.0)
+    assert c[0] == 3 and c[1] == 1 and c[255] == 1 and c.sum() == 5
+    r = oracle.histogram_range(x, np.array([0, 1, 4, 1024], np.float32))
+    assert r.tolist() == [2, 1, 2]
