@@ -57,6 +57,11 @@ WORKLOADS = {
                          desc="multisplit LSD radix sort, 2^28 uint32 keys, 6 x 5-bit + 1 x 2-bit"),
     "sort_pairs_r5": dict(n=1 << 28, pairs=True, kind="sort", m=32, bits=5, unit="Gpairs/s", bpe=140,
                           desc="multisplit LSD radix sort, 2^28 pairs, 6 x 5-bit + 1 x 2-bit"),
+    # device-wide histogram (Sec.7.3): 2^25 binary32 samples U[0,1024)
+    "hist_even": dict(n=1 << 25, pairs=False, kind="hist_even", m=256, unit="Gsamples/s", bpe=4,
+                      desc="device-wide Even histogram, 2^25 floats U[0,1024) (Sec.7.3, f2)"),
+    "hist_range": dict(n=1 << 25, pairs=False, kind="hist_range", m=256, unit="Gsamples/s", bpe=4,
+                       desc="device-wide Range histogram, 2^25 floats U[0,1024), m-1 random splitters (f2)"),
     "sort_keys_r4": dict(n=1 << 28, pairs=False, kind="sort", m=16, bits=4, unit="Gkeys/s", bpe=96,
                          desc="multisplit LSD radix sort, 2^28 uint32 keys, 8 x 4-bit"),
     "sort_pairs_r4": dict(n=1 << 28, pairs=True, kind="sort", m=16, bits=4, unit="Gpairs/s", bpe=160,
@@ -163,6 +168,12 @@ class Runner:
             bits = m.bit_length() - 1
             self.bucket = ms.Radix(0, bits)
             gdev.keys_(self.keys, SEED + rank, kind=gen.RADIX, m=m, shift=0, bits=bits, dist=dist, alpha=0.1)
+        elif kind.startswith("hist"):
+            import numpy as np
+            self.bucket = None
+            self.samples = torch.from_numpy(gen.floats(n, SEED + rank)).to(dev)
+            self.splitters = torch.from_numpy(gen.splitters(m, SEED)).to(dev)
+            self.counts = torch.empty(m, dtype=torch.int32, device=dev)
         else:  # sort
             self.bucket = None
             gdev.keys_(self.keys, SEED + rank)
@@ -185,7 +196,11 @@ class Runner:
             from paper_1701_01189_b200 import sharded
             self.ko, self.vo, _ = sharded.sharded_multisplit(keys, self.vals, self.bucket)
             return
-        if self.bucket is None:
+        if self.wl["kind"] == "hist_even":
+            self.ms.histogram_even(self.samples, self.m, 0.0, 1024.0, out=self.counts)
+        elif self.wl["kind"] == "hist_range":
+            self.ms.histogram_range(self.samples, self.splitters, out=self.counts)
+        elif self.bucket is None:
             self.ms.radix_sort(keys, self.vals, bits_per_pass=self.wl.get("bits", 8), out_keys=ko,
                                out_values=self.vo, workspace=self.ws)
         else:
@@ -238,6 +253,29 @@ def e2e_steps(run: Runner, steps: int, warmup: int):
     multisplit / sort, D2H of the outputs (and offsets), all inside the timed region."""
     import torch
     n = run.n
+    if run.wl["kind"].startswith("hist"):  # H2D of the samples, D2H of the m counts
+        xh = run.samples.cpu().pin_memory()
+        ch = torch.empty(run.m, dtype=torch.int32).pin_memory()
+        xd = torch.empty_like(run.samples)
+
+        def one_h():
+            xd.copy_(xh, non_blocking=True)
+            if run.wl["kind"] == "hist_even":
+                run.ms.histogram_even(xd, run.m, 0.0, 1024.0, out=run.counts)
+            else:
+                run.ms.histogram_range(xd, run.splitters, out=run.counts)
+            ch.copy_(run.counts, non_blocking=True)
+
+        for _ in range(max(1, warmup)):
+            one_h()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            one_h()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps, 4 * n, 4 * run.m
     kh = run.keys.cpu().pin_memory()
     vh = run.vals.cpu().pin_memory() if run.vals is not None else None
     koh = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -314,7 +352,13 @@ def run_ours(args, rank, world, local_rank):
     value = n * world / (ms_step * 1e-3) / 1e9  # all ranks' elements / max-over-ranks step time
     # dominant kernel = KF (kf_fused); algorithmic bytes per launch: read + write of keys (+ values)
     roofline = None
-    if stages is not None:
+    if wl["kind"].startswith("hist"):  # one kernel (kh_histogram) + a counts memset
+        achieved = 4 * n / (ms_step * 1e-3) / 1e9
+        roofline = {"kernel": "kh_histogram (warp-private smem counts + one global atomic per CTA and bucket)",
+                    "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(achieved / hbm, 4), "traffic": load_traffic(f"{args.workload}_m{m}"),
+                    "alg_bytes_per_launch": 4 * n, "peak_source": peak_src}
+    elif stages is not None:
         ks_bytes = n * (16 if wl["pairs"] else 8)
         achieved = ks_bytes / (stages["postscan"] * 1e-3) / 1e9
         # m <= 32: KM (prescan + per-(tile, warp) slot bases) -> KF kf_meta; otherwise
@@ -329,11 +373,12 @@ def run_ours(args, rank, world, local_rank):
     whole_frac = value * 1e9 / world * wl["bpe"] / (hbm * 1e9)
     e2e_ms, h2d, d2h = e2e_steps(run, max(3, args.steps // 4), 2)
     out = {
-        "metric": f"multisplit {wl['unit']} ({args.workload}, m={m})" if wl["kind"] != "sort"
+        "metric": (f"histogram {wl['unit']} ({args.workload}, m={m})" if wl["kind"].startswith("hist") else
+                   f"multisplit {wl['unit']} ({args.workload}, m={m})") if wl["kind"] != "sort"
         else f"radix sort {wl['unit']} ({args.workload})",
         "value": round(value, 3), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-        "scaling": "strong" if wl.get("strong") else "weak", "vs_baseline": None, "dtype": "u32",
+        "scaling": "strong" if wl.get("strong") else "weak", "vs_baseline": None, "dtype": "f32" if wl["kind"].startswith("hist") else "u32",
         "data": "synthetic (seeded counter-based generator)",
         "config": {"workload": wl["desc"], "n_per_rank": n, "n_total": n * world, "m": m, "bucket": wl["kind"],
                    "pairs": wl["pairs"], "l2": "flushed before every timed step (512 MiB write)",
@@ -361,7 +406,8 @@ def sweep(args, dev, flush, hbm):
     res = {}
     cases = [("ms_keys", m) for m in (2, 8, 32, 64, 256)] + [("ms_pairs", m) for m in (2, 8, 32, 256)] + \
             [("ms_pairs_c3", 64), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256), ("sort_keys", 256),
-             ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32)]
+             ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32), ("hist_even", 2),
+             ("hist_even", 256), ("hist_range", 2), ("hist_range", 256)]
     for name, m in cases:
         wl = WORKLOADS[name]
         run = Runner(wl, m, dev)
@@ -397,6 +443,13 @@ def _oracle_sample(wl, m, n_sample):
         fn = None
         k = gen.keys(n_sample, SEED)
     v = gen.values(n_sample, SEED, parity=False) if wl["pairs"] else None
+    if kind == "hist_even":
+        x = gen.floats(n_sample, SEED)
+        return lambda: oracle.histogram_even(x, m, 0.0, 1024.0)
+    if kind == "hist_range":
+        x = gen.floats(n_sample, SEED)
+        spl = gen.splitters(m, SEED)
+        return lambda: oracle.histogram_range(x, spl)
     if fn is None:
         return lambda: oracle.radix_sort(k, v)
     return lambda: oracle.multisplit(k, fn, v)
@@ -434,11 +487,12 @@ def run_reference(args, rank, world):
     dt = sum(ts) / len(ts)
     value = n_sample / dt / 1e9
     out = {"impl": "reference",
-           "metric": f"multisplit {wl['unit']} ({args.workload}, m={m})" if wl["kind"] != "sort"
+           "metric": (f"histogram {wl['unit']} ({args.workload}, m={m})" if wl["kind"].startswith("hist") else
+                   f"multisplit {wl['unit']} ({args.workload}, m={m})") if wl["kind"] != "sort"
            else f"radix sort {wl['unit']} ({args.workload})",
            "value": round(value, 4), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded counter-based generator)",
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl["kind"].startswith("hist") else "u32", "data": "synthetic (seeded counter-based generator)",
            "config": {"workload": wl["desc"], "n": wl["n"], "m": m, "bucket": wl["kind"], "pairs": wl["pairs"]},
            "cpu_baseline": {"value": round(value, 4), "unit": wl["unit"], "cores": 1, "kind": "oracle",
                             "sample": f"each step: {n_sample} elements of the workload (seed {SEED})"},

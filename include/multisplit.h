@@ -140,6 +140,27 @@ ms_status ms_radix_sort_pairs(const uint32_t *keys_in, const uint32_t *vals_in,
 int ms_radix_pass_schedule(uint32_t begin_bit, uint32_t end_bit, uint32_t bits_per_pass,
                            uint32_t *shifts, uint32_t *bits, int cap);
 
+/* ------------------------------------------------------------------------
+ * Device-wide histogram (Sec.7.3 "GPU Histogram"): counts[j] =
+ * number of samples in bucket j, j < m, m in 1..256.  `samples` (n binary32
+ * values) and `counts` (m words, overwritten) are device pointers; stream-
+ * ordered, no allocation, no synchronization.
+ *   ms_histogram_even:  m buckets of width Delta = (upper - lower) / m between
+ *     s_0 = lower and s_m = upper; bucket of x = floor((x - lower) /
+ *     Delta) in binary32 round-to-nearest, clamped to m-1; samples outside
+ *     [lower, upper) and NaN are not counted (readings R25-R26).
+ *     MS_ERR_INVALID_VALUE unless lower < upper.
+ *   ms_histogram_range: m+1 device splitters s_0 < s_1 < ... < s_m (strictly
+ *     increasing; not checked); bucket of x = j with s_j <= x < s_{j+1}
+ *     (upper-bound search); samples outside [s_0, s_m) not counted.
+ * Errors: MS_ERR_UNSUPPORTED for m outside 1..256 or n >= 2^32,
+ * MS_ERR_INVALID_VALUE for NULL pointers (samples may be NULL when n = 0).
+ * --------------------------------------------------------------------- */
+ms_status ms_histogram_even(const float *samples, uint64_t n, uint32_t m, float lower,
+                            float upper, uint32_t *counts, void *stream);
+ms_status ms_histogram_range(const float *samples, uint64_t n, uint32_t m,
+                             const float *splitters, uint32_t *counts, void *stream);
+
 /* Synchronizes `stream` and returns MS_ERR_KEY_DOMAIN if the most recent
  * multisplit that used `ws` saw an identity key >= m, else MS_SUCCESS. */
 ms_status ms_device_status(const void *ws, void *stream);

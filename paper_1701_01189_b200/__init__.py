@@ -197,3 +197,37 @@ def scan(H: torch.Tensor, stream=None):
     check(lib.ms_stage_scan(H.data_ptr(), G.data_ptr(), L, m, off.data_ptr(), ws.data_ptr(), ws.numel(),
                             _stream_ptr(stream)), "ms_stage_scan")
     return G, off
+
+
+def _f32view(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def histogram_even(samples: torch.Tensor, m: int, lower: float, upper: float, *,
+                   out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Device-wide Even histogram (Sec.7.3): counts[m] (int32 storage of uint32)."""
+    samples = _f32view(samples, "samples")
+    c = out if out is not None else torch.empty(m, dtype=torch.int32, device=samples.device)
+    st = _lib.load().ms_histogram_even(samples.data_ptr(), samples.numel(), m, float(lower), float(upper),
+                                       c.data_ptr(), _stream_ptr(stream))
+    check(st, "ms_histogram_even")
+    return c
+
+
+def histogram_range(samples: torch.Tensor, splitters: torch.Tensor, *, out: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+    """Device-wide Range histogram (Sec.7.3): counts[m] for m+1 splitters."""
+    samples = _f32view(samples, "samples")
+    splitters = _f32view(splitters, "splitters")
+    m = splitters.numel() - 1
+    c = out if out is not None else torch.empty(max(m, 1), dtype=torch.int32, device=samples.device)
+    st = _lib.load().ms_histogram_range(samples.data_ptr(), samples.numel(), m, splitters.data_ptr(),
+                                        c.data_ptr(), _stream_ptr(stream))
+    check(st, "ms_histogram_range")
+    return c

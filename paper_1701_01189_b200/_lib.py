@@ -56,6 +56,8 @@ SIGNATURES = [
     ("ms_shard_plan", _I, [_P, _U32, _U32, _U32, _P, _P, _P, _P, _P, _P]),
     ("ms_shard_merge_keys", _I, [_P, _U64, _FN, _P, _P, _U32, _P, _P]),
     ("ms_shard_merge_pairs", _I, [_P, _P, _U64, _FN, _P, _P, _U32, _P, _P, _P]),
+    ("ms_histogram_even", _I, [_P, _U64, _U32, ctypes.c_float, ctypes.c_float, _P, _P]),
+    ("ms_histogram_range", _I, [_P, _U64, _U32, _P, _P, _P]),
     ("ms_set_stage_events", None, [_P]),
     ("ms_launch_count", _U64, []),
 ]

@@ -9,6 +9,7 @@
 
 #include "../../include/multisplit.h"
 #include "ms_dispatch.cuh"
+#include "ms_hist.cuh"
 #include "ms_scan.cuh"
 
 using namespace ms;
@@ -498,6 +499,42 @@ ms_status ms_multisplit_pairs(const uint32_t *keys_in, const uint32_t *vals_in,
                               size_t ws_bytes, void *stream) {
   return multisplit_impl(keys_in, vals_in, keys_out, vals_out, n, fn, bucket_offsets, ws,
                          ws_bytes, stream, true);
+}
+
+// ---------------------------------------------------------------- histogram (Sec.7.3)
+static ms_status histogram_impl(const float *x, uint64_t n, uint32_t m, float lower, float upper,
+                                const float *splitters, uint32_t *counts, void *stream,
+                                bool range) {
+  if (m < 1 || m > 256) return MS_ERR_UNSUPPORTED;
+  if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
+  if (!counts || (n > 0 && !x) || (range && !splitters)) return MS_ERR_INVALID_VALUE;
+  if (!range && !(lower < upper)) return MS_ERR_INVALID_VALUE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(counts, 0, (size_t)m * 4u, s) != cudaSuccess) return MS_ERR_CUDA;
+  if (n == 0) return MS_SUCCESS;
+  volatile float delta = (upper - lower) / (float)m;  // binary32, round to nearest (R25)
+  const uint32_t target = (uint32_t)sm_count() * 2u;
+  uint32_t per = (uint32_t)((n + target - 1) / target);
+  per = (per + 4095u) & ~4095u;  // whole 16-byte vectors per CTA, >= 4096 samples
+  const uint32_t grid = (uint32_t)((n + per - 1) / per);
+  const size_t smem = ((size_t)kWarps * m + m + 1) * 4u;
+  if (range)
+    kh_histogram<true><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, 0.f, 0.f, 0.f,
+                                                    splitters, counts);
+  else
+    kh_histogram<false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, lower, upper, delta,
+                                                     nullptr, counts);
+  return counted(cudaGetLastError()) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+}
+
+ms_status ms_histogram_even(const float *samples, uint64_t n, uint32_t m, float lower,
+                            float upper, uint32_t *counts, void *stream) {
+  return histogram_impl(samples, n, m, lower, upper, nullptr, counts, stream, false);
+}
+
+ms_status ms_histogram_range(const float *samples, uint64_t n, uint32_t m,
+                             const float *splitters, uint32_t *counts, void *stream) {
+  return histogram_impl(samples, n, m, 0.f, 0.f, splitters, counts, stream, true);
 }
 
 int ms_radix_pass_schedule(uint32_t begin_bit, uint32_t end_bit, uint32_t r, uint32_t *shifts,

@@ -1,0 +1,94 @@
+// ms_hist.cuh -- device-wide histogram (Sec.7.3 "GPU Histogram"):
+// the multisplit's prescan with the per-subproblem histograms summed into one
+// global histogram instead of stored for a scan.  As the paper chose (option
+// 2): each CTA (a contiguous range of samples, one per SM slot)
+// counts into warp-private shared-memory rows (the warp-level privatization
+// of P:1941-1943, here with shared-memory increments, measured cheapest on
+// B200 for the multisplit prescan) and adds its m totals to the global
+// histogram with one atomicAdd per bucket.
+//
+//   Even: b = floor((x - s_0) / Delta), Delta = (s_m - s_0) / m,
+//                   binary32 round-to-nearest (reading R25), a
+//                   quotient of m clamped to m-1, x outside [s_0, s_m) or NaN
+//                   not counted (reading R26).
+//   Range: splitters s_0 < ... < s_m staged in shared memory (P:1960-
+//                   1962); b = upper_bound(s, x) - 1 by a branch-free binary
+//                   search of ceil(log2 m) steps.
+#pragma once
+#include "ms_device.cuh"
+
+namespace ms {
+
+template <bool RANGE>
+__device__ __forceinline__ void hist_sample(float v, uint32_t m, float lower, float upper,
+                                            float delta, const float *spl, uint32_t *row) {
+  uint32_t b;
+  if constexpr (RANGE) {
+    if (!(v >= spl[0] && v < spl[m])) return;
+    uint32_t j = 0;  // largest j with spl[j] <= v (spl[0] <= v < spl[m])
+#pragma unroll
+    for (uint32_t step = 128; step >= 1; step >>= 1)
+      if (j + step < m && spl[j + step] <= v) j += step;
+    b = j;
+  } else {
+    if (!(v >= lower && v < upper)) return;
+    const float q = __fdiv_rn(__fsub_rn(v, lower), delta);
+    b = (uint32_t)floorf(q);
+    b = b < m - 1 ? b : m - 1;
+  }
+  atomicAdd(row + b, 1u);
+}
+
+template <bool RANGE>
+__global__ void __launch_bounds__(kThreads, 2)
+    kh_histogram(const float *__restrict__ x, uint32_t n, uint32_t elems_per_cta, uint32_t m,
+                 float lower, float upper, float delta, const float *__restrict__ splitters,
+                 uint32_t *__restrict__ counts) {
+  extern __shared__ uint32_t hg_smem[];  // cnt[kWarps][m] | splitters[m+1]
+  uint32_t *cnt = hg_smem;
+  float *spl = reinterpret_cast<float *>(hg_smem + kWarps * m);
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < kWarps * m; i += kThreads) cnt[i] = 0u;
+  if constexpr (RANGE)
+    for (uint32_t i = tid; i <= m; i += kThreads) spl[i] = __ldg(splitters + i);
+  __syncthreads();
+  uint32_t *row = cnt + (tid >> 5) * m;
+  const uint32_t lo = blockIdx.x * elems_per_cta;
+  const uint32_t hi = (uint32_t)min((uint64_t)n, (uint64_t)lo + elems_per_cta);
+  uint32_t i = lo;
+  if ((reinterpret_cast<uintptr_t>(x + lo) & 15u) == 0) {
+    const uint4 *v = reinterpret_cast<const uint4 *>(x + lo);
+    const uint32_t nv = (hi - lo) >> 2;
+    uint32_t j = tid;
+    for (; j + 7u * kThreads < nv; j += 8u * kThreads) {  // 8 x 16 B in flight per thread
+      uint4 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[u] = ldg_stream_v4(v + j + (uint32_t)u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        hist_sample<RANGE>(__uint_as_float(q[u].x), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE>(__uint_as_float(q[u].y), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE>(__uint_as_float(q[u].z), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE>(__uint_as_float(q[u].w), m, lower, upper, delta, spl, row);
+      }
+    }
+    for (; j < nv; j += kThreads) {
+      const uint4 q = ldg_stream_v4(v + j);
+      hist_sample<RANGE>(__uint_as_float(q.x), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE>(__uint_as_float(q.y), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE>(__uint_as_float(q.z), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE>(__uint_as_float(q.w), m, lower, upper, delta, spl, row);
+    }
+    i = lo + (nv << 2);
+  }
+  for (i += tid; i < hi; i += kThreads) hist_sample<RANGE>(__ldg(x + i), m, lower, upper, delta, spl, row);
+  __syncthreads();
+  for (uint32_t b = tid; b < m; b += kThreads) {
+    uint32_t s = 0;
+#pragma unroll 4
+    for (int w = 0; w < kWarps; ++w) s += cnt[w * m + b];
+    if (s) atomicAdd(counts + b, s);
+  }
+}
+
+}  // namespace ms
