@@ -3,6 +3,7 @@
 // radix-sort pass driver.  All launches are stream-ordered; nothing here
 // synchronizes except ms_device_status.
 #include <atomic>
+#include <cmath>
 #include <vector>
 #include <cstdlib>
 #include <cstring>
@@ -367,6 +368,13 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
   if (meta_mode) {  // KF reduces the range histograms itself (no KR)
     stage_event(2, s);
+    // reverse tile order (+ MS_KM_KEEP evict_last tiles): parity-green, measured
+    // within noise of the forward order, so opt-in
+    static const int rev_env = [] {
+      const char *v = std::getenv("MS_KF_REVERSE");
+      return v ? std::atoi(v) : 0;
+    }();
+    a.reverse = rev_env != 0;
     a.mode = kModeRange;
     a.R = H;
     a.tiles_per_cta = K;
@@ -518,12 +526,18 @@ static ms_status histogram_impl(const float *x, uint64_t n, uint32_t m, float lo
   per = (per + 4095u) & ~4095u;  // whole 16-byte vectors per CTA, >= 4096 samples
   const uint32_t grid = (uint32_t)((n + per - 1) / per);
   const size_t smem = ((size_t)kWarps * m + m + 1) * 4u;
+  int ex = 0;
+  const bool pow2 = std::frexp((float)delta, &ex) == 0.5f && std::isnormal((float)delta) &&
+                    std::isnormal(1.0f / (float)delta);
   if (range)
-    kh_histogram<true><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, 0.f, 0.f, 0.f,
-                                                    splitters, counts);
+    kh_histogram<true, false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, 0.f, 0.f, 0.f,
+                                                           splitters, counts);
+  else if (pow2)  // exact: multiply by the power-of-two reciprocal
+    kh_histogram<false, true><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, lower, upper,
+                                                           1.0f / (float)delta, nullptr, counts);
   else
-    kh_histogram<false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, lower, upper, delta,
-                                                     nullptr, counts);
+    kh_histogram<false, false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, lower, upper,
+                                                            delta, nullptr, counts);
   return counted(cudaGetLastError()) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
 }
 

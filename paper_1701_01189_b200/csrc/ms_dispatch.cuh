@@ -10,7 +10,27 @@
 
 namespace ms {
 
+// L2 prefetch distance (tiles) of KM beyond its TMA ring (MS_KM_PREFETCH; default 0:
+// 2 and 4 measured slower)
+inline uint32_t km_prefetch() {
+  static const uint32_t v = [] {
+    const char *e = std::getenv("MS_KM_PREFETCH");
+    return e ? (uint32_t)std::atoi(e) : 0u;
+  }();
+  return v;
+}
+
 // MS_META_RANK=atomic selects the shared-memory atomicOr peer masks in kf_meta
+// Tiles at the end of each KM range loaded with an L2 evict_last policy, for
+// KF's reverse tile order (MS_KM_KEEP, default 0; with MS_KF_REVERSE=1)
+inline uint32_t km_keep_last() {
+  static const uint32_t v = [] {
+    const char *e = std::getenv("MS_KM_KEEP");
+    return e ? (uint32_t)std::atoi(e) : 0u;
+  }();
+  return v;
+}
+
 // Whether this GPU returns same-address shared-memory increments in lane order
 // (RANK 8); probed once per process on a private stream (ms_capi.cu).
 bool lane_ordered_inc();
@@ -137,14 +157,14 @@ cudaError_t Launch<KIND>::tile_meta(bool pairs, const uint32_t *keys, uint32_t n
   }
   if (bp.m <= 2) {
     if (pairs)
-      km_tile_meta<KIND, true, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, true, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
     else
-      km_tile_meta<KIND, true, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, true, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
   } else {
     if (pairs)
-      km_tile_meta<KIND, false, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, false, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
     else
-      km_tile_meta<KIND, false, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+      km_tile_meta<KIND, false, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
   }
   return cudaGetLastError();
 }

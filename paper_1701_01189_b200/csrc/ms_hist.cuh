@@ -19,7 +19,9 @@
 
 namespace ms {
 
-template <bool RANGE>
+// POW2 (Even, Delta a power of two): x / Delta and x * (1 / Delta) are the same
+// correctly rounded binary32 value, so the division becomes a multiply.
+template <bool RANGE, bool POW2 = false>
 __device__ __forceinline__ void hist_sample(float v, uint32_t m, float lower, float upper,
                                             float delta, const float *spl, uint32_t *row) {
   uint32_t b;
@@ -32,14 +34,14 @@ __device__ __forceinline__ void hist_sample(float v, uint32_t m, float lower, fl
     b = j;
   } else {
     if (!(v >= lower && v < upper)) return;
-    const float q = __fdiv_rn(__fsub_rn(v, lower), delta);
+    const float q = POW2 ? __fmul_rn(__fsub_rn(v, lower), delta) : __fdiv_rn(__fsub_rn(v, lower), delta);
     b = (uint32_t)floorf(q);
     b = b < m - 1 ? b : m - 1;
   }
   atomicAdd(row + b, 1u);
 }
 
-template <bool RANGE>
+template <bool RANGE, bool POW2>
 __global__ void __launch_bounds__(kThreads, 2)
     kh_histogram(const float *__restrict__ x, uint32_t n, uint32_t elems_per_cta, uint32_t m,
                  float lower, float upper, float delta, const float *__restrict__ splitters,
@@ -66,22 +68,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int u = 0; u < 8; ++u) q[u] = ldg_stream_v4(v + j + (uint32_t)u * kThreads);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        hist_sample<RANGE>(__uint_as_float(q[u].x), m, lower, upper, delta, spl, row);
-        hist_sample<RANGE>(__uint_as_float(q[u].y), m, lower, upper, delta, spl, row);
-        hist_sample<RANGE>(__uint_as_float(q[u].z), m, lower, upper, delta, spl, row);
-        hist_sample<RANGE>(__uint_as_float(q[u].w), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE, POW2>(__uint_as_float(q[u].x), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE, POW2>(__uint_as_float(q[u].y), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE, POW2>(__uint_as_float(q[u].z), m, lower, upper, delta, spl, row);
+        hist_sample<RANGE, POW2>(__uint_as_float(q[u].w), m, lower, upper, delta, spl, row);
       }
     }
     for (; j < nv; j += kThreads) {
       const uint4 q = ldg_stream_v4(v + j);
-      hist_sample<RANGE>(__uint_as_float(q.x), m, lower, upper, delta, spl, row);
-      hist_sample<RANGE>(__uint_as_float(q.y), m, lower, upper, delta, spl, row);
-      hist_sample<RANGE>(__uint_as_float(q.z), m, lower, upper, delta, spl, row);
-      hist_sample<RANGE>(__uint_as_float(q.w), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE, POW2>(__uint_as_float(q.x), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE, POW2>(__uint_as_float(q.y), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE, POW2>(__uint_as_float(q.z), m, lower, upper, delta, spl, row);
+      hist_sample<RANGE, POW2>(__uint_as_float(q.w), m, lower, upper, delta, spl, row);
     }
     i = lo + (nv << 2);
   }
-  for (i += tid; i < hi; i += kThreads) hist_sample<RANGE>(__ldg(x + i), m, lower, upper, delta, spl, row);
+  for (i += tid; i < hi; i += kThreads) hist_sample<RANGE, POW2>(__ldg(x + i), m, lower, upper, delta, spl, row);
   __syncthreads();
   for (uint32_t b = tid; b < m; b += kThreads) {
     uint32_t s = 0;

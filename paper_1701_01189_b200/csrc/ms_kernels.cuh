@@ -247,6 +247,7 @@ struct KfArgs {
   int carry;       // per-element scatter: hold each bucket's partial trailing sector back
                    // in shared memory until the range's next tile completes it
   uint32_t carry_m;  // m (carry array stride)
+  int reverse;       // kf_meta: tiles of the range from the last one down
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),

@@ -57,7 +57,8 @@ template <int KIND, bool SMALLM, int ITEMS>
 __global__ void __launch_bounds__(kThreads + 32, 2)
     km_tile_meta(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
-                 uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+                 uint32_t *__restrict__ R, uint32_t *__restrict__ hdr, uint32_t prefetch_ahead,
+                 uint32_t keep_last) {
   constexpr uint32_t W = kWarps;
   constexpr uint32_t SL = 32u * ITEMS;  // keys per warp slice
   constexpr uint32_t T = W * SL;
@@ -89,13 +90,20 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 
   if (warp == W) {
     // ============================ scan warp ===================================
+    auto prefetch = [&](uint32_t t) {  // beyond the ring: into L2 ahead of the TMA load
+      if (lane == 0 && t < t1 && via_tma(t)) prefetch_l2_bulk(keys + (size_t)t * T, T * 4u);
+    };
     auto issue = [&](uint32_t t, uint32_t st) {
       if (lane == 0 && t < t1 && via_tma(t)) {
+        // the range's last keep_last tiles stay in L2 for KF, which starts there
+        const uint64_t pol = t + keep_last >= t1 ? policy_evict_last() : policy_evict_first();
         mbar_arrive_expect_tx(&full[st], T * 4u);
-        tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], policy_evict_first());
+        tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], pol);
       }
+      prefetch(t + prefetch_ahead);
     };
     for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
+    for (uint32_t i = KS; i < KS + prefetch_ahead; ++i) prefetch(t0 + i);
     uint32_t running = 0;  // range count of bucket lane
     uint32_t k = 0;
     for (uint32_t t = t0; t < t1; ++t, ++k) {
@@ -265,6 +273,10 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
   const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
   if (t0 >= t1) return;
+  // iteration k handles tile(k): forward, or (a.reverse) from the range's last
+  // tile down -- KM has just read the range's last tiles, still in L2
+  const uint32_t nt = t1 - t0;
+  auto tile = [&](uint32_t k) { return k >= nt ? t1 : (a.reverse ? t1 - 1 - k : t0 + k); };
   auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
   auto via_tma = [&](uint32_t t) { return a.use_tma && tile_n(t) == T; };
   // one elected thread starts the TMA bulk copies of a tile: the input data
@@ -293,10 +305,10 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       prefetch_l2_bulk(a.meta + (size_t)t * MS, MS * 4u);
     }
   };
-  auto issue = [&](uint32_t t, uint32_t st) {
-    issue_data(t, st);
-    issue_meta(t, st);
-    prefetch(t + a.prefetch_ahead);
+  auto issue = [&](uint32_t k, uint32_t st) {
+    issue_data(tile(k), st);
+    issue_meta(tile(k), st);
+    prefetch(tile(k + a.prefetch_ahead));
   };
   if (tid == 0) {
     for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
@@ -304,17 +316,16 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       for (uint32_t i = 0; i < kStages; ++i) mbar_init(&placed[i], NT);
   }
   __syncthreads();
-  issue_data(t0, 0);
-  issue_data(t0 + 1, 1);
+  issue_data(tile(0), 0);
+  issue_data(tile(1), 1);
   if constexpr (PROD) {
     if (warp == W) {
       // ======================= producer warp =================================
       griddep_wait();  // meta records are complete
-      issue_meta(t0, 0);
-      issue_meta(t0 + 1, 1);
-      for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(t0 + j);
-      uint32_t k = 0;
-      for (uint32_t t = t0; t < t1; ++t, ++k) {
+      issue_meta(tile(0), 0);
+      issue_meta(tile(1), 1);
+      for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(tile(j));
+      for (uint32_t k = 0; k < nt; ++k) {
         const uint32_t st = k % kStages;
         uint32_t *s_stage = stage0 + st * SW;
         const uint32_t *tab = s_tab + st * 96u;
@@ -323,7 +334,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         bulk_wait_read();
         __syncwarp();
         if (lane == 0) fence_proxy_async_smem();
-        issue(t + 2, (k + 2) % kStages);
+        issue(k + 2, (k + 2) % kStages);
         mbar_wait(&placed[st], (k / kStages) & 1u);
         // one TMA bulk store per bucket run body (16-byte aligned), then the
         // <= 3 leading / trailing elements of every run with plain stores
@@ -397,9 +408,9 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   // then forms base[b] + P[c][b] for its bucket lanes.  R is G m words, read
   // from L2 (11 MB in all at m = 32, G = 296).
   griddep_wait();  // KM complete: meta records and range histograms
-  issue_meta(t0, 0);
-  issue_meta(t0 + 1, 1);
-  for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(t0 + j);
+  issue_meta(tile(0), 0);
+  issue_meta(tile(1), 1);
+  for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(tile(j));
   uint32_t gbase = 0, grun = 0;
   {
     uint32_t *red = s_mask;  // [2][16][32] scratch (the mask rows are zeroed per tile)
@@ -439,19 +450,20 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     }
     if (lane < m) {
       gbase = incl - tot + pre;
+      if (a.reverse) grun = __ldg(a.R + (size_t)c * m + lane);  // the range's bucket total
       if (c == 0 && warp == 0 && a.bucket_offsets) {
         a.bucket_offsets[lane] = incl - tot;
         if (lane == m - 1) a.bucket_offsets[m] = incl;
       }
     }
   }
-  load_tile(t0, 0);
+  load_tile(tile(0), 0);
   named_barrier_sync(1, NT);
 
   uint32_t *mrow0 = s_mask + warp * 32, *mrow1 = s_mask + (W + warp) * 32,
            *mrow2 = s_mask + (2 * W + warp) * 32;
-  uint32_t k = 0;
-  for (uint32_t t = t0; t < t1; ++t, ++k) {
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint32_t t = tile(k);
     const uint32_t st = k % kStages;
     uint32_t *s_stage = stage0 + st * SW;
     const uint32_t *rec = s_stage + MO;
@@ -467,8 +479,11 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       const uint32_t sbw = rec[warp * mS + lane];
       const uint32_t tb = rec[lane];
       const uint32_t te = lane + 1 < m ? rec[lane + 1] : tn;
-      const uint32_t gs = gbase + grun;  // Eq.3 term 3: tiles before this one in the range
-      grun += te - tb;
+      // Eq.3 term 3: the range's tiles before this one (reverse: grun counts down
+      // from the range total)
+      if (a.reverse) grun -= te - tb;
+      const uint32_t gs = gbase + grun;
+      if (!a.reverse) grun += te - tb;
       const uint32_t adj = a.store_runs ? 4u * lane + ((gs - tb) & 3u) : 0u;
       wrun = sbw + adj;
       if (warp == W - 1) {
@@ -633,11 +648,11 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     }
     if constexpr (PROD) {
       mbar_arrive(&placed[st]);  // tile t placed: the producer may store it
-      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      if (k + 1 < nt) load_tile(tile(k + 1), k + 1);
       named_barrier_sync(1, NT);
     } else if (a.store_runs) {
       // ---- next tile's keys into registers before the barrier -----------------
-      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      if (k + 1 < nt) load_tile(tile(k + 1), k + 1);
       named_barrier_sync(1, NT);
       // ---- run stores of tile t: one TMA bulk store per run body by the last
       // warp, the <= 3 leading / trailing elements by threads 8b .. 8b+7
@@ -677,11 +692,11 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         bulk_wait_read_newest_pending();
         __syncwarp();
         if (lane == 0) fence_proxy_async_smem();
-        issue(t + 2, (k + 2) % kStages);
+        issue(k + 2, (k + 2) % kStages);
       }
     } else {
       // ---- next tile's keys into registers before the barrier -----------------
-      if (t + 1 < t1) load_tile(t + 1, k + 1);
+      if (k + 1 < nt) load_tile(tile(k + 1), k + 1);
       named_barrier_sync(1, NT);
       // ---- coalesced scatter of tile t: slot s of bucket b -> delta[b] + s ----
       const uint32_t s0 = wbase + lane;
@@ -705,7 +720,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       if (warp == W - 1) {
         __syncwarp();
         if (lane == 0) fence_proxy_async_smem();
-        issue(t + 2, (k + 2) % kStages);
+        issue(k + 2, (k + 2) % kStages);
       }
     }
   }

@@ -25,3 +25,14 @@ def test_rank_mode_parity(rank, prod):
     r = subprocess.run([sys.executable, os.path.join(HERE, "_rank_mode_check.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"MS_KF_REVERSE": "1", "MS_KM_KEEP": "4"}, {"MS_KF_PREFETCH": "0"},
+                                 {"MS_KM_PREFETCH": "2"}, {"MS_NO_META": "1"}, {"MS_NO_RANK_INC": "1"},
+                                 {"MS_NO_RUN_STORES": "1"}])
+def test_pipeline_options_parity(env):
+    """Measured-and-rejected or fallback pipeline options stay bit-exact."""
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "_rank_mode_check.py")], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
