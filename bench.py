@@ -89,7 +89,7 @@ def load_traffic(key):
 class ClockSampler:
     """Samples SM clock + throttle reasons with NVML in a thread during the timed region."""
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period, self.index = period_s, index
         self._stop = threading.Event()
@@ -337,9 +337,9 @@ def run_ours(args, rank, world, local_rank):
         # serialize the programmatic dependent launches); a separate pass below
         # records the per-stage breakdown for the roofline of the postscan
         times, _, launches = time_steps(run, args.steps, args.warmup, flush, stage_events=False)
-    stages = None
-    if world == 1:
-        _, stages, _ = time_steps(run, max(3, args.steps // 2), 1, flush, stage_events=True)
+        stages = None
+        if world == 1:
+            _, stages, _ = time_steps(run, max(3, args.steps // 2), 1, flush, stage_events=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -503,7 +503,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)  # the paper averages 50 trials
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="ms_keys")

@@ -417,16 +417,17 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     const uint32_t G = a.num_ranges, c = blockIdx.x;
     uint32_t pre = 0, tot = 0;
     if (lane < m) {
-      // batches of 8 independent loads (rows warp, warp + W, ...)
-      for (uint32_t r0 = warp; r0 < G; r0 += 8 * W) {
-        uint32_t v[8];
+      // batches of 20 independent loads (rows warp, warp + W, ...): one batch
+      // covers G <= 320 ranges (2 CTAs on 148 SMs: G = 296)
+      for (uint32_t r0 = warp; r0 < G; r0 += 20 * W) {
+        uint32_t v[20];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 20; ++j) {
           const uint32_t r = r0 + j * W;
           v[j] = r < G ? __ldg(a.R + (size_t)r * m + lane) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 20; ++j) {
           tot += v[j];
           pre += r0 + j * W < c ? v[j] : 0u;
         }

@@ -82,6 +82,17 @@ def test_tile_size():
         [T, T // 2, T, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2, T // 2]
 
 
+@pytest.mark.parametrize("k", [(1, -1), (1, 0), (1, 1), (2, -3), (3, 5), (37, 4097)])
+@pytest.mark.parametrize("m", [2, 5, 32, 33, 256])
+def test_tile_boundaries_keys(k, m):
+    """key-only inputs at exact multiples of the keys tile (ms.tile_size) +- a ragged tail"""
+    Tk = ms.tile_size(m, False)
+    n = k[0] * Tk + k[1]
+    ob, pb, gk = bucket_pair("delta", m)
+    keys = gen.keys(n, seed=n + m, dist=gen.DIST_UNIFORM, **gk)
+    check_multisplit(keys, None, ob, pb)
+
+
 @pytest.mark.parametrize("n", [T - 1, T, T + 1, 2 * T - 3, 3 * T + 5, 37 * T + 4097])
 @pytest.mark.parametrize("m", [2, 5, 32, 33, 64, 200, 256])
 @pytest.mark.parametrize("dist", [gen.DIST_UNIFORM, gen.DIST_SKEW, gen.DIST_BINOMIAL])
