@@ -302,6 +302,12 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
       return v ? (uint32_t)std::atoi(v) : 2u;
     }();
     a.prefetch_ahead = pf;
+    // evict_last on the L2 prefetches (measured +1-3.5 % at m = 32); MS_KF_PREFETCH_KEEP=0 off
+    static const bool keep = [] {
+      const char *v = std::getenv("MS_KF_PREFETCH_KEEP");
+      return !(v && !std::strcmp(v, "0"));
+    }();
+    a.prefetch_keep = keep;
     static const bool inc_off = env_flag("MS_NO_RANK_INC");
     // measured (profiles/r01/s2_summary.md): increments win for keys and for
     // m <= 32; peer masks for pairs with m > 32

@@ -176,6 +176,14 @@ __device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gmem_src
 __device__ __forceinline__ void prefetch_l2_bulk(const void *gmem, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
 }
+// the same with an L2 cache policy (e.g. evict_last: keep the lines until their
+// TMA load, ahead of the streaming output)
+__device__ __forceinline__ void prefetch_l2_bulk_hint(const void *gmem, uint32_t bytes,
+                                                      uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(gmem),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
 
 // 1-D bulk copy shared -> global (TMA store, SASS UBLKCP).  Addresses and size
 // must be multiples of 16 bytes; completion is tracked with bulk groups.

@@ -248,6 +248,7 @@ struct KfArgs {
                    // in shared memory until the range's next tile completes it
   uint32_t carry_m;  // m (carry array stride)
   int reverse;       // kf_meta: tiles of the range from the last one down
+  int prefetch_keep; // kf_meta: L2 prefetches with an evict_last policy
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),

@@ -300,9 +300,16 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   // into L2 so that their TMA loads later see L2 latency, not DRAM latency
   auto prefetch = [&](uint32_t t) {
     if (tid == kProducer && t < t1 && via_tma(t)) {
-      prefetch_l2_bulk(a.keys_in + (size_t)t * T, T * 4u);
-      if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)t * T, T * 4u);
-      prefetch_l2_bulk(a.meta + (size_t)t * MS, MS * 4u);
+      if (a.prefetch_keep) {
+        const uint64_t pol = policy_evict_last();
+        prefetch_l2_bulk_hint(a.keys_in + (size_t)t * T, T * 4u, pol);
+        if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)t * T, T * 4u, pol);
+        prefetch_l2_bulk_hint(a.meta + (size_t)t * MS, MS * 4u, pol);
+      } else {
+        prefetch_l2_bulk(a.keys_in + (size_t)t * T, T * 4u);
+        if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)t * T, T * 4u);
+        prefetch_l2_bulk(a.meta + (size_t)t * MS, MS * 4u);
+      }
     }
   };
   auto issue = [&](uint32_t k, uint32_t st) {
