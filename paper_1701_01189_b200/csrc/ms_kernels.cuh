@@ -769,8 +769,14 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       // tiles beyond the three-stage ring: into L2 ahead of their TMA loads
       const uint32_t tp = t + a.prefetch_ahead;
       if (a.mode == kModeRange && a.prefetch_ahead && tp < t1 && tile_n(tp) == T) {
-        prefetch_l2_bulk(a.keys_in + (size_t)tp * T, T * 4u);
-        if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)tp * T, T * 4u);
+        if (a.prefetch_keep) {
+          const uint64_t kp = policy_evict_last();
+          prefetch_l2_bulk_hint(a.keys_in + (size_t)tp * T, T * 4u, kp);
+          if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)tp * T, T * 4u, kp);
+        } else {
+          prefetch_l2_bulk(a.keys_in + (size_t)tp * T, T * 4u);
+          if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)tp * T, T * 4u);
+        }
       }
     }
   };
