@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
   if (warp == W) {
     // ============================ scan warp ===================================
     auto prefetch = [&](uint32_t t) {  // beyond the ring: into L2 ahead of the TMA load
-      if (lane == 0 && t < t1 && via_tma(t)) prefetch_l2_bulk(keys + (size_t)t * T, T * 4u);
+      if (lane == 0 && t < t1 && via_tma(t))
+        prefetch_l2_bulk_hint(keys + (size_t)t * T, T * 4u, policy_evict_last());
     };
     auto issue = [&](uint32_t t, uint32_t st) {
       if (lane == 0 && t < t1 && via_tma(t)) {
