@@ -10,10 +10,14 @@
  *    32-bit words (keys unsigned, values opaque payload).
  *  - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t
  *    passed as void*; NULL = legacy default stream).  No call allocates
- *    memory, synchronizes, or copies to the host, except ms_device_status.
+ *    memory, synchronizes, or copies to the host, except ms_device_init /
+ *    ms_lane_ordered_increment (one-time probe), ms_device_status, and the
+ *    NCCL path of the sharded calls (documented there).  Every multisplit /
+ *    sort call can be captured in a CUDA graph.
  *  - The caller owns every buffer.  Workspace is queried with the matching
- *    *_workspace_size function and passed in; one workspace serves one
- *    in-flight call.  Inputs are never modified.  Outputs must not alias
+ *    *_workspace_size function (pure host arithmetic) and passed in; it must
+ *    be 256-byte aligned (else MS_ERR_INVALID_VALUE; cudaMalloc and torch
+ *    allocations are); one workspace serves one in-flight call.  Inputs are never modified.  Outputs must not alias
  *    inputs (P:785-787 key_in / key_out are distinct).
  *  - Host-detectable argument errors return before anything is launched.
  *    Device-detected key-domain errors (identity bucket with key >= m) set
@@ -62,16 +66,42 @@ const char *ms_status_string(ms_status s);
 /* Library version, e.g. "0.1.0". */
 const char *ms_version(void);
 
-/* 1 if the current GPU returns the old values of one warp instruction's
- * same-address shared-memory increments in lane order, else 0.  For m >= 3
- * the postscan ranks a window's keys with such increments of the warp's
- * running slot per bucket (Eq.4 term 1); stability needs the lane
- * order, so the library probes it once per process (one 32-thread kernel on a
- * private stream, synchronous) and otherwise ranks with peer masks.  Called
- * implicitly by ms_multisplit_workspace_size() and the first m >= 3 call;
- * call it (or the workspace query) before capturing a CUDA graph.  Errors:
- * any CUDA failure of the probe reads as 0. */
+/* One-time, per-device initialisation (synchronous; call it once per device
+ * before use and outside any CUDA graph capture; idempotent and thread-safe;
+ * device < 0 = the current device).  It runs the probe of reading R23
+ * (DESIGN.md): whether the GPU returns the old values of one warp
+ * instruction's same-address shared-memory increments in lane order, and
+ * applies consecutive increments of a warp in program order -- checked over
+ * the whole grid in the postscan's own launch shape (512 threads, two CTAs per
+ * SM) with random, sorted-run, 90 %-skewed and two-bucket patterns over up to
+ * 256 counters.  Where the probe held, the postscan ranks a window's keys with
+ * such increments of the warp's running slot (Eq.4 term 1); on a
+ * device that has not been initialised, or where the probe failed, it ranks
+ * with deterministic peer masks (Alg.3's peer masks).  Results are
+ * identical either way; only speed differs.  MS_ERR_CUDA on a CUDA failure. */
+ms_status ms_device_init(int device);
+
+/* The probe result for the current device (runs the probe if needed, as
+ * ms_device_init does): 1 = lane-ordered, 0 = not (or a CUDA failure). */
 int ms_lane_ordered_increment(void);
+
+/* Process-wide options (thread-safe; they apply to calls issued afterwards).
+ *   MS_OPT_RANK:       MS_RANK_AUTO (default: increments where the device's
+ *                      probe held) or MS_RANK_PEER_MASKS (always the
+ *                      deterministic peer masks).
+ *   MS_OPT_RUN_STORES: 1 (default: whole-run TMA bulk stores where runs are
+ *                      long) or 0 (per-element coalesced stores only).
+ *   MS_OPT_PIPELINE:   MS_PIPELINE_LEVEL0 (default: Eq.3 with the CTA ranges
+ *                      as level 0, two launches) or MS_PIPELINE_TILE (the
+ *                      paper's {tile histograms H, scan of H, postscan},
+ *                      P:529-540, three launches).
+ * ms_set_option returns MS_ERR_INVALID_VALUE for an unknown option / value;
+ * ms_get_option returns the value, or -1 for an unknown option. */
+enum { MS_OPT_RANK = 0, MS_OPT_RUN_STORES = 1, MS_OPT_PIPELINE = 2 };
+enum { MS_RANK_AUTO = 0, MS_RANK_PEER_MASKS = 1 };
+enum { MS_PIPELINE_LEVEL0 = 0, MS_PIPELINE_TILE = 1 };
+ms_status ms_set_option(int option, int value);
+int ms_get_option(int option);
 
 /* Fill *out with delta buckets of width ceil(2^32 / m) (2^32-1 for m = 1),
  * the equal-width partition of the key domain of P:1107. */

@@ -21,7 +21,7 @@ from ._lib import MultisplitError, check, ms_bucket_fn
 
 __all__ = ["Bucket", "Delta", "Identity", "Radix", "multisplit", "radix_sort", "device_status",
            "prescan", "scan", "tile_size", "radix_pass_schedule", "workspace_size",
-           "MultisplitError"]
+           "set_option", "get_option", "device_init", "MultisplitError"]
 
 
 @dataclass(frozen=True)
@@ -56,19 +56,63 @@ def Radix(shift: int, bits: int) -> Bucket:
     return Bucket(_lib.MS_BUCKET_RADIX, 1 << bits, shift=shift, bits=bits)
 
 
-def _u32view(t: torch.Tensor, name: str) -> torch.Tensor:
+def _u32view(t: torch.Tensor, name: str, device: torch.device | None = None,
+             numel: int | None = None) -> torch.Tensor:
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
     if t.dtype not in (torch.int32, torch.uint32):
         raise TypeError(f"{name} must be int32 or uint32, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs {numel}")
     return t
 
 
-def _stream_ptr(stream) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _workspace(ws, need: int, device: torch.device) -> torch.Tensor:
+    if ws is None or ws.numel() < need:
+        return torch.empty(max(need, 1), dtype=torch.uint8, device=device)
+    if not ws.is_cuda or ws.device != device or not ws.is_contiguous() or ws.data_ptr() % 256:
+        raise ValueError("workspace must be a contiguous, 256-byte aligned tensor on the keys' device")
+    return ws
+
+
+_initialised: set[int] = set()
+
+
+def device_init(device: torch.device | int | None = None) -> None:
+    """ms_device_init: the one-time per-device probe (synchronous; outside graph capture)."""
+    if device is None:
+        idx = torch.cuda.current_device()
+    elif isinstance(device, int):
+        idx = device
+    else:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _initialised:
+        check(_lib.load().ms_device_init(idx), "ms_device_init")
+        _initialised.add(idx)
+
+
+def _prepare(t: torch.Tensor) -> None:
+    """Per-call device guard: the library launches on the current device."""
+    if t.device.index is not None and t.device.index not in _initialised:
+        device_init(t.device.index)
+
+
+def _stream_ptr(stream, device: torch.device | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
+
+
+def set_option(option: int, value: int) -> None:
+    """ms_set_option (process-wide): MS_OPT_RANK / MS_OPT_RUN_STORES / MS_OPT_PIPELINE."""
+    check(_lib.load().ms_set_option(option, value), "ms_set_option")
+
+
+def get_option(option: int) -> int:
+    return int(_lib.load().ms_get_option(option))
 
 
 def workspace_size(n: int, m: int, with_values: bool) -> int:
@@ -85,23 +129,34 @@ def multisplit(keys: torch.Tensor, values: torch.Tensor | None = None, bucket: B
         raise ValueError("bucket is required (Delta / Identity / Radix)")
     lib = _lib.load()
     keys = _u32view(keys, "keys")
+    dv = keys.device
     n = keys.numel()
     pairs = values is not None
     if pairs:
-        values = _u32view(values, "values")
+        values = _u32view(values, "values", dv)
         if values.numel() != n:
             raise ValueError("keys and values differ in length")
-    ko = out_keys if out_keys is not None else torch.empty_like(keys)
-    vo = (out_values if out_values is not None else torch.empty_like(values)) if pairs else None
+    ko = _u32view(out_keys, "out_keys", dv, n) if out_keys is not None else torch.empty_like(keys)
+    vo = None
+    if pairs:
+        vo = _u32view(out_values, "out_values", dv, n) if out_values is not None else torch.empty_like(values)
     off = out_offsets
     if off is None and offsets:
-        off = torch.empty(bucket.m + 1, dtype=torch.int32, device=keys.device)
+        off = torch.empty(bucket.m + 1, dtype=torch.int32, device=dv)
+    elif off is not None:
+        off = _u32view(off, "out_offsets", dv, bucket.m + 1)
     need = lib.ms_multisplit_workspace_size(n, bucket.m, int(pairs))
-    ws = workspace
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=keys.device)
+    ws = _workspace(workspace, need, dv)
     fn = bucket.c()
-    sp = _stream_ptr(stream)
+    _prepare(keys)
+    with torch.cuda.device(dv):
+        sp = _stream_ptr(stream, dv)
+        _call_multisplit(lib, pairs, keys, values, ko, vo, n, fn, off, ws, sp)
+    multisplit.last_workspace = ws
+    return ko, vo, off
+
+
+def _call_multisplit(lib, pairs, keys, values, ko, vo, n, fn, off, ws, sp):
     if pairs:
         st = lib.ms_multisplit_pairs(keys.data_ptr(), values.data_ptr(), ko.data_ptr(), vo.data_ptr(),
                                      n, ctypes.byref(fn), off.data_ptr() if off is not None else None,
@@ -111,8 +166,6 @@ def multisplit(keys: torch.Tensor, values: torch.Tensor | None = None, bucket: B
                                     off.data_ptr() if off is not None else None,
                                     ws.data_ptr(), ws.numel(), sp)
     check(st, "ms_multisplit_pairs" if pairs else "ms_multisplit_keys")
-    multisplit.last_workspace = ws
-    return ko, vo, off
 
 
 def device_status(workspace: torch.Tensor | None = None, stream=None) -> int:
@@ -131,23 +184,28 @@ def radix_sort(keys: torch.Tensor, values: torch.Tensor | None = None, *, begin_
     bits_per_pass = 0: the library's choice (5-bit digits, see include/multisplit.h)."""
     lib = _lib.load()
     keys = _u32view(keys, "keys")
+    dv = keys.device
     n = keys.numel()
     pairs = values is not None
     if pairs:
-        values = _u32view(values, "values")
-    ko = out_keys if out_keys is not None else torch.empty_like(keys)
-    vo = (out_values if out_values is not None else torch.empty_like(values)) if pairs else None
-    need = lib.ms_radix_sort_workspace_size(n, int(pairs))
-    ws = workspace
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=keys.device)
-    sp = _stream_ptr(stream)
+        values = _u32view(values, "values", dv)
+        if values.numel() != n:
+            raise ValueError("keys and values differ in length")
+    ko = _u32view(out_keys, "out_keys", dv, n) if out_keys is not None else torch.empty_like(keys)
+    vo = None
     if pairs:
-        st = lib.ms_radix_sort_pairs(keys.data_ptr(), values.data_ptr(), ko.data_ptr(), vo.data_ptr(), n,
-                                     begin_bit, end_bit, bits_per_pass, ws.data_ptr(), ws.numel(), sp)
-    else:
-        st = lib.ms_radix_sort_keys(keys.data_ptr(), ko.data_ptr(), n, begin_bit, end_bit, bits_per_pass,
-                                    ws.data_ptr(), ws.numel(), sp)
+        vo = _u32view(out_values, "out_values", dv, n) if out_values is not None else torch.empty_like(values)
+    need = lib.ms_radix_sort_workspace_size(n, int(pairs))
+    ws = _workspace(workspace, need, dv)
+    _prepare(keys)
+    with torch.cuda.device(dv):
+        sp = _stream_ptr(stream, dv)
+        if pairs:
+            st = lib.ms_radix_sort_pairs(keys.data_ptr(), values.data_ptr(), ko.data_ptr(), vo.data_ptr(), n,
+                                         begin_bit, end_bit, bits_per_pass, ws.data_ptr(), ws.numel(), sp)
+        else:
+            st = lib.ms_radix_sort_keys(keys.data_ptr(), ko.data_ptr(), n, begin_bit, end_bit, bits_per_pass,
+                                        ws.data_ptr(), ws.numel(), sp)
     check(st, "ms_radix_sort_pairs" if pairs else "ms_radix_sort_keys")
     return ko, vo
 

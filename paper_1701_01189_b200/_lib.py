@@ -19,6 +19,14 @@ MS_ERR_CUDA = 4
 MS_ERR_KEY_DOMAIN = 5
 MS_ERR_NCCL = 6
 
+MS_OPT_RANK = 0
+MS_OPT_RUN_STORES = 1
+MS_OPT_PIPELINE = 2
+MS_RANK_AUTO = 0
+MS_RANK_PEER_MASKS = 1
+MS_PIPELINE_LEVEL0 = 0
+MS_PIPELINE_TILE = 1
+
 MS_BUCKET_IDENTITY = 0
 MS_BUCKET_DELTA = 1
 MS_BUCKET_RADIX = 2
@@ -37,6 +45,9 @@ SIGNATURES = [
     ("ms_status_string", ctypes.c_char_p, [_I]),
     ("ms_version", ctypes.c_char_p, []),
     ("ms_lane_ordered_increment", _I, []),
+    ("ms_device_init", _I, [_I]),
+    ("ms_set_option", _I, [_I, _I]),
+    ("ms_get_option", _I, [_I]),
     ("ms_bucket_delta_default", _I, [_U32, _FN]),
     ("ms_bucket_identity", _I, [_U32, _FN]),
     ("ms_bucket_radix", _I, [_U32, _U32, _FN]),

@@ -3,6 +3,7 @@
 // radix-sort pass driver.  All launches are stream-ordered; nothing here
 // synchronizes except ms_device_status.
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <vector>
 #include <cstdlib>
@@ -16,24 +17,67 @@
 using namespace ms;
 
 namespace ms {
-// RANK 8 probe (see k_probe_lane_ordered_inc): runs once, synchronously, on a
-// private stream at the first m <= 32 multisplit of the process.
-bool lane_ordered_inc() {
-  static const bool ok = [] {
-    uint32_t *d = nullptr, h = 0;
-    cudaStream_t st = nullptr;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return false;
-    bool r = false;
-    if (cudaMallocAsync((void **)&d, 4, st) == cudaSuccess) {
-      k_probe_lane_ordered_inc<<<1, 32, 0, st>>>(d);
-      r = cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-          cudaFreeAsync(d, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess && h == 1u;
-    }
-    cudaStreamDestroy(st);
-    return r;
-  }();
-  return ok;
+// Reading R23 probe per device (k_probe_lane_ordered_inc, ms_meta.cuh): -1 not
+// yet run, 0 failed, 1 held.  Run only by ms_device_init / ms_lane_ordered_increment
+// (synchronous, on a private stream); a multisplit on a device that has not
+// been probed ranks with the deterministic peer masks.
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_probe[kMaxDevices];
+std::mutex g_probe_mu;
+std::atomic<int> g_opt[3] = {{MS_RANK_AUTO}, {1}, {MS_PIPELINE_LEVEL0}};
+
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) return -1;
+  return d;
 }
+
+int run_probe() {
+  int sms = 0, dev = current_device();
+  if (dev < 0 || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  const size_t smem = kfm_smem_bytes(32, false);  // the postscan's footprint: 2 CTAs per SM
+  if (cudaFuncSetAttribute(k_probe_lane_ordered_inc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return 0;
+  uint32_t *d = nullptr, h = 0, one = 1;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return 0;
+  bool r = false;
+  if (cudaMallocAsync((void **)&d, 4, st) == cudaSuccess) {
+    r = cudaMemcpyAsync(d, &one, 4, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    if (r) {
+      k_probe_lane_ordered_inc<<<2 * sms, kThreads, smem, st>>>(d, 64u);
+      r = cudaGetLastError() == cudaSuccess &&
+          cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    }
+    r = cudaFreeAsync(d, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess && r &&
+        h == 1u;
+  }
+  cudaStreamDestroy(st);
+  return r ? 1 : 0;
+}
+
+// the probe result of the current device, running it if `run` and not yet done
+int lane_ordered_inc(bool run) {
+  const int dev = current_device();
+  if (dev < 0) return 0;
+  int v = g_probe[dev].load(std::memory_order_acquire);
+  if (v >= 0 || !run) return v;
+  std::lock_guard<std::mutex> lk(g_probe_mu);
+  v = g_probe[dev].load(std::memory_order_acquire);
+  if (v < 0) {
+    v = run_probe();
+    g_probe[dev].store(v, std::memory_order_release);
+  }
+  return v;
+}
+
+struct ProbeInit {
+  ProbeInit() {
+    for (auto &p : g_probe) p.store(-1);
+  }
+} g_probe_init;
 }  // namespace ms
 
 namespace {
@@ -74,14 +118,6 @@ struct Layout {
   uint32_t T, L, nchunks, C, MS;
 };
 
-// m <= 32: the prescan writes per-tile meta records (ms_meta.cuh) unless disabled
-bool use_meta(uint32_t m) {
-  static const bool off = [] {
-    const char *v = std::getenv("MS_NO_META");
-    return v && *v && std::strcmp(v, "0") != 0;
-  }();
-  return m <= 32 && !off;
-}
 
 Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   Layout lo{};
@@ -99,7 +135,7 @@ Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   lo.status = lo.H + align_up((size_t)lo.L * m * 8u);  // H (or R and its prefixes P)
   lo.total = lo.status + align_up((size_t)lo.nchunks * m * 8u);
   lo.meta = lo.total;
-  if (m <= 32) {  // tile meta records (sized whether or not MS_NO_META is set)
+  if (m <= 32) {  // tile meta records (ms_meta.cuh)
     lo.MS = meta_stride(meta_ms(m), kWarps);
     lo.total = lo.meta + align_up((size_t)lo.L * lo.MS * 4u);
   }
@@ -166,15 +202,6 @@ int sm_count() {
   return n;
 }
 
-bool env_flag(const char *name) {
-  const char *v = std::getenv(name);
-  return v && *v && std::strcmp(v, "0") != 0;
-}
-
-bool three_launch_mode() {
-  const char *v = std::getenv("MS_PIPELINE");
-  return v && !std::strcmp(v, "3pass");
-}
 
 cudaError_t launch_level0_scan(const uint32_t *R, uint32_t *P, uint32_t *Tot, uint32_t G,
                                uint32_t m, cudaStream_t s) {
@@ -259,7 +286,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   if (st != MS_SUCCESS) return st;
   if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
   const uint32_t m = fn->num_buckets;
-  if (!ws) return MS_ERR_INVALID_VALUE;
+  if (!ws || ((uintptr_t)ws & (kAlign - 1))) return MS_ERR_INVALID_VALUE;
   if (n > 0) {
     if (!keys_in || !keys_out) return MS_ERR_INVALID_VALUE;
     if (pairs && (!vals_in || !vals_out)) return MS_ERR_INVALID_VALUE;
@@ -294,25 +321,14 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   // whole-run TMA bulk stores pay off when the average bucket run of a tile is
   // >= 256 elements (measured: profiles/r01/); shorter runs use per-element stores
   a.store_runs = m <= 64 && lo.T / m >= 256u && (((uintptr_t)keys_out & 15u) == 0) &&
-                 (!pairs || (((uintptr_t)vals_out & 15u) == 0)) && !env_flag("MS_NO_RUN_STORES");
-
-  {
-    static const uint32_t pf = [] {
-      const char *v = std::getenv("MS_KF_PREFETCH");
-      return v ? (uint32_t)std::atoi(v) : 2u;
-    }();
-    a.prefetch_ahead = pf;
-    // evict_last on the L2 prefetches (measured +1-3.5 % at m = 32); MS_KF_PREFETCH_KEEP=0 off
-    static const bool keep = [] {
-      const char *v = std::getenv("MS_KF_PREFETCH_KEEP");
-      return !(v && !std::strcmp(v, "0"));
-    }();
-    a.prefetch_keep = keep;
-    static const bool inc_off = env_flag("MS_NO_RANK_INC");
-    // measured (profiles/r01/s2_summary.md): increments win for keys and for
-    // m <= 32; peer masks for pairs with m > 32
-    a.rank_inc = m > 2 && (!pairs || m <= 32) && !inc_off && ms::lane_ordered_inc();
-  }
+                 (!pairs || (((uintptr_t)vals_out & 15u) == 0)) &&
+                 g_opt[MS_OPT_RUN_STORES].load(std::memory_order_relaxed) != 0;
+  // Eq.4 term 1 by lane-ordered increments (reading R23) only on a device whose
+  // probe passed and unless deterministic peer masks are requested; measured
+  // (profiles/r01/s2_summary.md): increments win for keys and for m <= 32
+  a.rank_inc = m > 2 && (!pairs || m <= 32) &&
+               g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
+               ms::lane_ordered_inc(false) == 1;
 
   if (n <= lo.T) {  // one subproblem: a single launch
     a.mode = kModeSingle;
@@ -330,7 +346,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   uint32_t *H = (uint32_t *)(w + lo.H);
   a.num_tiles = lo.L;
 
-  if (three_launch_mode()) {
+  if (g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed) == MS_PIPELINE_TILE) {
     // paper-faithful {local, global, local}: tile histograms H -> scan -> postscan
     unsigned long long *status = (unsigned long long *)(w + lo.status);
     stage_event(0, s);
@@ -360,7 +376,7 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
   const uint32_t K = (lo.L + target - 1) / target;
   const uint32_t G = (lo.L + K - 1) / K;
-  const bool meta_mode = use_meta(m);
+  const bool meta_mode = m <= 32;
   uint32_t *meta = (uint32_t *)(w + lo.meta);
   stage_event(0, s);
   if (meta_mode) {
@@ -374,13 +390,6 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
   if (meta_mode) {  // KF reduces the range histograms itself (no KR)
     stage_event(2, s);
-    // reverse tile order (+ MS_KM_KEEP evict_last tiles): parity-green, measured
-    // within noise of the forward order, so opt-in
-    static const int rev_env = [] {
-      const char *v = std::getenv("MS_KF_REVERSE");
-      return v ? std::atoi(v) : 0;
-    }();
-    a.reverse = rev_env != 0;
     a.mode = kModeRange;
     a.R = H;
     a.tiles_per_cta = K;
@@ -397,13 +406,6 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   a.Tot = base;
   a.tiles_per_cta = K;
   a.num_ranges = G;
-  {
-    // per-element scatter holding back partial trailing sectors: correct but
-    // measured 1.1-1.8x slower, so opt-in via MS_CARRY=1
-    static const bool carry_env = env_flag("MS_CARRY");
-    a.carry = carry_env && m > 32 && !a.store_runs;
-    a.carry_m = m;
-  }
   const cudaError_t e = counted(fused(pl, pairs, a, G, s));
   stage_event(3, s);
   return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
@@ -416,7 +418,7 @@ ms_status radix_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
   const int passes = ms_radix_pass_schedule(begin_bit, end_bit, r, shifts, bits, 32);
   if (passes < 0) return MS_ERR_INVALID_VALUE;
   if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
-  if (!ws) return MS_ERR_INVALID_VALUE;
+  if (!ws || ((uintptr_t)ws & (kAlign - 1))) return MS_ERR_INVALID_VALUE;
   if (n == 0) return MS_SUCCESS;
   if (!keys_in || !keys_out || (pairs && (!vals_in || !vals_out))) return MS_ERR_INVALID_VALUE;
   if (overlaps(keys_in, keys_out, n)) return MS_ERR_INVALID_VALUE;
@@ -467,7 +469,37 @@ const char *ms_status_string(ms_status s) {
 
 const char *ms_version(void) { return "0.1.0"; }
 
-int ms_lane_ordered_increment(void) { return ms::lane_ordered_inc() ? 1 : 0; }
+int ms_lane_ordered_increment(void) { return ms::lane_ordered_inc(true) == 1 ? 1 : 0; }
+
+ms_status ms_device_init(int device) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return MS_ERR_CUDA;
+  if (device >= 0 && device != prev && cudaSetDevice(device) != cudaSuccess) return MS_ERR_CUDA;
+  const int r = ms::lane_ordered_inc(true);
+  if (device >= 0 && device != prev) cudaSetDevice(prev);
+  return r < 0 ? MS_ERR_CUDA : MS_SUCCESS;
+}
+
+ms_status ms_set_option(int option, int value) {
+  switch (option) {
+    case MS_OPT_RANK:
+      if (value != MS_RANK_AUTO && value != MS_RANK_PEER_MASKS) return MS_ERR_INVALID_VALUE;
+      break;
+    case MS_OPT_RUN_STORES:
+      if (value != 0 && value != 1) return MS_ERR_INVALID_VALUE;
+      break;
+    case MS_OPT_PIPELINE:
+      if (value != MS_PIPELINE_LEVEL0 && value != MS_PIPELINE_TILE) return MS_ERR_INVALID_VALUE;
+      break;
+    default: return MS_ERR_INVALID_VALUE;
+  }
+  ms::g_opt[option].store(value, std::memory_order_relaxed);
+  return MS_SUCCESS;
+}
+
+int ms_get_option(int option) {
+  return option >= 0 && option < 3 ? ms::g_opt[option].load(std::memory_order_relaxed) : -1;
+}
 
 ms_status ms_bucket_delta_default(uint32_t m, ms_bucket_fn *out) {
   if (!out) return MS_ERR_INVALID_VALUE;
@@ -494,7 +526,6 @@ ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out) {
 ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn); }
 
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
-  if (m >= 3 && n > 0) (void)ms::lane_ordered_inc();  // probe outside any capture
   if (m < 1) m = 1;
   if (m > 256) m = 256;
   return layout_for(n, m, with_values != 0).total;

@@ -8,48 +8,23 @@
 
 #include "ms_meta.cuh"
 
+#include <atomic>
+
 namespace ms {
 
-// L2 prefetch distance (tiles) of KM beyond its TMA ring (MS_KM_PREFETCH; default 0:
-// 2 and 4 measured slower)
-inline uint32_t km_prefetch() {
-  static const uint32_t v = [] {
-    const char *e = std::getenv("MS_KM_PREFETCH");
-    return e ? (uint32_t)std::atoi(e) : 0u;
-  }();
-  return v;
-}
-
-// MS_META_RANK=atomic selects the shared-memory atomicOr peer masks in kf_meta
-// Tiles at the end of each KM range loaded with an L2 evict_last policy, for
-// KF's reverse tile order (MS_KM_KEEP, default 0; with MS_KF_REVERSE=1)
-inline uint32_t km_keep_last() {
-  static const uint32_t v = [] {
-    const char *e = std::getenv("MS_KM_KEEP");
-    return e ? (uint32_t)std::atoi(e) : 0u;
-  }();
-  return v;
-}
-
-// Whether this GPU returns same-address shared-memory increments in lane order
-// (RANK 8); probed once per process on a private stream (ms_capi.cu).
-bool lane_ordered_inc();
-
-// kf_meta's RANK for m buckets: MS_META_RANK = atomic | ballot | mix3 | mix2 |
-// xatomic | xmix3 | xmix2 overrides; by default the choice measured best per
-// number of bucket bits (profiles/r01/s2_rank_modes.md)
-inline int meta_rank_mode(uint32_t m) {
-  static const int forced = [] {
-    const char *e = std::getenv("MS_META_RANK");
-    if (!e) return -1;
-    const char *names[] = {"atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2", "xpair", "inc"};
-    for (int i = 0; i < 9; ++i)
-      if (!std::strcmp(e, names[i])) return i;
-    return -1;
-  }();
-  if (forced >= 0) return forced;
-  if (lane_ordered_inc()) return 8;
-  return m <= 8 ? 6 : (m <= 16 ? 5 : 7);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current
+// device only: each kernel instantiation keeps one bit per device (thread-safe;
+// setting the attribute twice is harmless).
+template <typename K>
+inline cudaError_t set_max_smem(K kern, size_t bytes, std::atomic<unsigned long long> &done) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+  const unsigned long long bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 template <int KIND>
@@ -116,19 +91,16 @@ template <int KIND, bool PAIRS, bool SMALLM, int CLS, int SCAN>
 static cudaError_t kf_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
   constexpr KfShape sh = kf_shape(PAIRS, CLS);
   auto kern = kf_fused<KIND, PAIRS, SMALLM, sh.warps, sh.items, sh.ctas_per_sm, SCAN>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kf_smem_bytes(CLS == 0 ? 32 : (CLS == 1 ? 64 : kMaxBuckets), PAIRS, false, true));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t e0 =
+      set_max_smem(kern, kf_smem_bytes(CLS == 0 ? 32 : (CLS == 1 ? 64 : kMaxBuckets), PAIRS, false), done);
+  if (e0 != cudaSuccess) return e0;
   // programmatic dependent launch: the prologue (barrier init, TMA of the first
   // tiles) overlaps the tail of the previous kernel; griddep_wait() orders the rest
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(sh.warps * 32);
-  cfg.dynamicSmemBytes = kf_smem_bytes(bp.m, PAIRS, a.rank_inc != 0, a.carry != 0);
+  cfg.dynamicSmemBytes = kf_smem_bytes(bp.m, PAIRS, a.rank_inc != 0);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -145,40 +117,26 @@ cudaError_t Launch<KIND>::tile_meta(bool pairs, const uint32_t *keys, uint32_t n
                                     const BucketParams &bp, uint32_t *meta, uint32_t *R,
                                     uint32_t *hdr, cudaStream_t s) {
   const size_t smem = km_smem_bytes(bp.m, pairs);
-  static bool configured = false;
-  if (!configured) {
-    for (auto kern : {km_tile_meta<KIND, true, 8>, km_tile_meta<KIND, false, 8>,
-                      km_tile_meta<KIND, true, 16>, km_tile_meta<KIND, false, 16>}) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(km_smem_bytes(32, false) > km_smem_bytes(32, true) ? km_smem_bytes(32, false) : km_smem_bytes(32, true)));
-      if (e != cudaSuccess) return e;
-    }
-    configured = true;
-  }
-  if (bp.m <= 2) {
-    if (pairs)
-      km_tile_meta<KIND, true, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
-    else
-      km_tile_meta<KIND, true, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
-  } else {
-    if (pairs)
-      km_tile_meta<KIND, false, 8><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
-    else
-      km_tile_meta<KIND, false, 16><<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr, km_prefetch(), km_keep_last());
-  }
-  return cudaGetLastError();
+  const size_t smax = km_smem_bytes(32, false) > km_smem_bytes(32, true) ? km_smem_bytes(32, false)
+                                                                          : km_smem_bytes(32, true);
+  static std::atomic<unsigned long long> done[4];
+  auto go = [&](auto kern, int i) {
+    const cudaError_t e = set_max_smem(kern, smax, done[i]);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads + 32, smem, s>>>(keys, n, num_tiles, tiles_per_cta, bp, meta, R, hdr);
+    return cudaGetLastError();
+  };
+  if (bp.m <= 2)
+    return pairs ? go(km_tile_meta<KIND, true, 8>, 0) : go(km_tile_meta<KIND, true, 16>, 1);
+  return pairs ? go(km_tile_meta<KIND, false, 8>, 2) : go(km_tile_meta<KIND, false, 16>, 3);
 }
 
 template <int KIND, bool PAIRS, bool SMALLM, int RANK, bool PROD>
 static cudaError_t kfm_go2(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
   auto kern = kf_meta<KIND, PAIRS, SMALLM, PAIRS ? 8 : 16, RANK, PROD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kfm_smem_bytes(32, PAIRS));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t e = set_max_smem(kern, kfm_smem_bytes(32, PAIRS), done);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(PROD ? kThreads + 32 : kThreads);
@@ -192,15 +150,11 @@ static cudaError_t kfm_go2(const KfArgs &a, const BucketParams &bp, uint32_t gri
   return cudaLaunchKernelEx(&cfg, kern, a, bp);
 }
 
-// whole-run TMA bulk stores -> producer-warp variant; per-element scatter otherwise
+// whole-run TMA bulk stores with a producer warp: measured faster for m <= 16,
+// slower at m = 32 (profiles/r01/); per-element scatter otherwise
 template <int KIND, bool PAIRS, bool SMALLM, int RANK>
 static cudaError_t kfm_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
-  // producer warp: measured faster for m <= 16, slower at m = 32 (profiles/r01/)
-  static const int prod_env = [] {
-    const char *e = std::getenv("MS_META_PROD");
-    return e ? std::atoi(e) : -1;
-  }();
-  const bool prod = a.store_runs && (prod_env >= 0 ? prod_env != 0 : bp.m <= 16);
+  const bool prod = a.store_runs && bp.m <= 16;
   return prod ? kfm_go2<KIND, PAIRS, SMALLM, RANK, true>(a, bp, grid, s)
               : kfm_go2<KIND, PAIRS, SMALLM, RANK, false>(a, bp, grid, s);
 }
@@ -209,21 +163,13 @@ template <int KIND>
 cudaError_t Launch<KIND>::fused_meta(bool pairs, const KfArgs &a, const BucketParams &bp,
                                      uint32_t grid, cudaStream_t s) {
   if (bp.m <= 2)
-    return pairs ? kfm_go<KIND, true, true, 0>(a, bp, grid, s) : kfm_go<KIND, false, true, 0>(a, bp, grid, s);
-#define MS_KFM_CASE(R) \
-  case R: return pairs ? kfm_go<KIND, true, false, R>(a, bp, grid, s) : kfm_go<KIND, false, false, R>(a, bp, grid, s)
-  switch (meta_rank_mode(bp.m)) {
-    MS_KFM_CASE(0);
-    MS_KFM_CASE(1);
-    MS_KFM_CASE(3);
-    MS_KFM_CASE(4);
-    MS_KFM_CASE(5);
-    MS_KFM_CASE(6);
-    MS_KFM_CASE(7);
-    MS_KFM_CASE(8);
-    default: return pairs ? kfm_go<KIND, true, false, 2>(a, bp, grid, s) : kfm_go<KIND, false, false, 2>(a, bp, grid, s);
-  }
-#undef MS_KFM_CASE
+    return pairs ? kfm_go<KIND, true, true, kRankBallot>(a, bp, grid, s)
+                 : kfm_go<KIND, false, true, kRankBallot>(a, bp, grid, s);
+  if (a.rank_inc)
+    return pairs ? kfm_go<KIND, true, false, kRankInc>(a, bp, grid, s)
+                 : kfm_go<KIND, false, false, kRankInc>(a, bp, grid, s);
+  return pairs ? kfm_go<KIND, true, false, kRankMasks>(a, bp, grid, s)
+               : kfm_go<KIND, false, false, kRankMasks>(a, bp, grid, s);
 }
 
 template <int KIND>

@@ -242,13 +242,7 @@ struct KfArgs {
   int mode;
   int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
-  uint32_t prefetch_ahead;  // L2 bulk prefetch distance (tiles) beyond each TMA load
-  int rank_inc;    // rank by lane-ordered shared-memory increments (ms_lane_ordered_increment)
-  int carry;       // per-element scatter: hold each bucket's partial trailing sector back
-                   // in shared memory until the range's next tile completes it
-  uint32_t carry_m;  // m (carry array stride)
-  int reverse;       // kf_meta: tiles of the range from the last one down
-  int prefetch_keep; // kf_meta: L2 prefetches with an evict_last policy
+  int rank_inc;    // rank by lane-ordered shared-memory increments (reading R23, probed per device)
 };
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),
@@ -281,8 +275,7 @@ __host__ __device__ constexpr uint32_t kf_out_slots(uint32_t T, uint32_t m) {
 // | per-warp counts [W][m] | per-warp running slots [W][m] (m <= 64) | delta[m]
 // | run table [3][m] (m <= 64)
 // (inc: ranking by lane-ordered increments, no peer-mask rows)
-__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs, bool inc = false,
-                                                bool carry = false) {
+__host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs, bool inc = false) {
   const int cls = kf_class(m);
   const size_t T = kf_tile(pairs, cls), W = (size_t)kf_shape(pairs, cls).warps;
   const size_t k = pairs ? 2u : 1u;
@@ -290,32 +283,7 @@ __host__ __device__ inline size_t kf_smem_bytes(uint32_t m, bool pairs, bool inc
   const size_t mrows = inc ? 0 : (cls == 0 ? 3 : 2);
   const size_t rows = mrows + (cls == 2 ? 1 : 2);  // masks + counts (+ slots)
   const size_t tables = cls == 2 ? 1 : 4;
-  // carry: sector end per bucket + up to 8 held-back elements per bucket (keys, values)
-  const size_t carry_words = carry ? mm + 8 * mm * k : 0;
-  return 3 * (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 + tables * mm * 4 +
-         carry_words * 4;
-}
-
-// Per-element scatter with carry (kModeRange): a CTA writes each bucket's part of
-// its range sequentially, tile after tile, so the sector that a tile's run ends
-// in is completed by the next tile's run.  The run's elements from its last
-// sector boundary fe = (gs + len) & ~7 on wait in s_carry[b][pos & 7]; when a
-// later run crosses the next boundary, the held-back elements [gs & ~7, gs)
-// are written together with it (never before the CTA's own first position).
-// Called by the one thread that owns bucket b, after the previous tile's
-// scatter and before this tile's.
-template <typename A>
-__device__ __forceinline__ void carry_in(const A &a, uint32_t b, uint32_t gs, uint32_t e,
-                                         uint32_t own, uint32_t *s_fe, uint32_t *s_carry) {
-  const uint32_t m = a.carry_m;
-  const uint32_t fe = e & ~7u, cs = gs & ~7u;
-  s_fe[b] = fe;
-  if (fe > cs) {
-    for (uint32_t p = max(cs, own); p < gs; ++p) {
-      a.keys_out[p] = s_carry[b * 8u + (p & 7u)];
-      if (a.vals_out) a.vals_out[p] = s_carry[m * 8u + b * 8u + (p & 7u)];
-    }
-  }
+  return 3 * (size_t)kf_out_slots((uint32_t)T, m) * k * 4 + rows * W * mm * 4 + tables * mm * 4;
 }
 
 // SCAN = 1 (m <= 32) / 2 (m <= 64): every warp scans the m x W tile counts
@@ -328,9 +296,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
                                            uint32_t tn, uint32_t *s_stage, uint32_t OS,
                                            uint32_t *s_mask, uint32_t *s_cnt,
                                            uint32_t *s_base, uint32_t *s_delta, uint32_t *s_run,
-                                           uint32_t *s_wsum, uint32_t (&running)[2],
-                                           uint32_t *s_fe, uint32_t *s_carry,
-                                           const uint32_t (&own)[2]) {
+                                           uint32_t *s_wsum, uint32_t (&running)[2]) {
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
   constexpr bool WSCAN = SCAN != 0;
@@ -462,7 +428,6 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
             s_run[2 * m + b] = tot[k];
           } else {
             s_delta[b] = gs - tb;
-            if (a.carry) carry_in(a, b, gs, gs + tot[k], own[k], s_fe, s_carry);
           }
         }
       }
@@ -542,7 +507,6 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
       }
     } else if (tid < m) {
       s_delta[tid] = gs - tb;
-      if (a.carry) carry_in(a, tid, gs, gs + (te - tb), own[0], s_fe, s_carry);
     }
   }
   __syncthreads();  // bucket threads have read warp 0's bases before it starts placing
@@ -679,38 +643,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
     uint32_t key[ITEMS], pos[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) key[i] = out_k[s0 + 32 * i];
-    if (a.carry) {
-      // elements at or past their bucket's last sector boundary wait in s_carry
-      uint32_t cb[ITEMS];
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        const uint32_t b = bucket_of<KIND>(key[i], bp);
-        cb[i] = b;
-        pos[i] = s_delta[b] + s0 + 32 * i;
-      }
-#pragma unroll
-      for (int i = 0; i < ITEMS; ++i) {
-        if (!valid_at(i)) continue;
-        if (pos[i] >= s_fe[cb[i]]) {
-          s_carry[cb[i] * 8u + (pos[i] & 7u)] = key[i];
-          cb[i] |= 0x80000000u;  // held back
-        } else {
-          a.keys_out[pos[i]] = key[i];
-        }
-      }
-      if constexpr (PAIRS) {
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) key[i] = out_v[s0 + 32 * i];
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          if (!valid_at(i)) continue;
-          if (cb[i] & 0x80000000u)
-            s_carry[m * 8u + (cb[i] & 0x7FFFFFFFu) * 8u + (pos[i] & 7u)] = key[i];
-          else
-            a.vals_out[pos[i]] = key[i];
-        }
-      }
-    } else {
+    {
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) pos[i] = s_delta[bucket_of<KIND>(key[i], bp)] + s0 + 32 * i;
 #pragma unroll
@@ -747,8 +680,6 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   uint32_t *s_base = s_cnt + W * mm;  // WSCAN only
   uint32_t *s_delta = WSCAN ? s_base + W * mm : s_base;
   uint32_t *s_run = s_delta + mm;
-  uint32_t *s_fe = s_delta + (SCAN == 0 ? 1u : 4u) * mm;  // carry: after the tables
-  uint32_t *s_carry = s_fe + mm;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr uint32_t kProducer = NT - 32;  // lane 0 of the last warp issues the TMA loads
 
@@ -766,17 +697,12 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
       tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
       if constexpr (PAIRS) tma_load_1d(dst + OS, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
-      // tiles beyond the three-stage ring: into L2 ahead of their TMA loads
-      const uint32_t tp = t + a.prefetch_ahead;
-      if (a.mode == kModeRange && a.prefetch_ahead && tp < t1 && tile_n(tp) == T) {
-        if (a.prefetch_keep) {
-          const uint64_t kp = policy_evict_last();
-          prefetch_l2_bulk_hint(a.keys_in + (size_t)tp * T, T * 4u, kp);
-          if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)tp * T, T * 4u, kp);
-        } else {
-          prefetch_l2_bulk(a.keys_in + (size_t)tp * T, T * 4u);
-          if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)tp * T, T * 4u);
-        }
+      // tiles beyond the three-stage ring: into L2 (evict_last) ahead of their TMA loads
+      const uint32_t tp = t + 2;
+      if (a.mode == kModeRange && tp < t1 && tile_n(tp) == T) {
+        const uint64_t kp = policy_evict_last();
+        prefetch_l2_bulk_hint(a.keys_in + (size_t)tp * T, T * 4u, kp);
+        if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)tp * T, T * 4u, kp);
       }
     }
   };
@@ -831,7 +757,6 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       running[0] = s_delta[tid];
     }
   }
-  const uint32_t own[2] = {running[0], running[1]};  // first positions of the range's buckets
 
   // ---- tiles of this range, in order; three stages rotate through
   //      TMA load -> count/place in place -> stores ----------------------------
@@ -852,11 +777,11 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     if (tn == T)
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, true>(a, bp, t, tn, s_stage, OS, s_mask,
                                                             s_cnt, s_base, s_delta, s_run, s_wsum,
-                                                            running, s_fe, s_carry, own);
+                                                            running);
     else
       kf_do_tile<KIND, PAIRS, SMALLM, W, ITEMS, SCAN, false>(a, bp, t, tn, s_stage, OS, s_mask,
                                                              s_cnt, s_base, s_delta, s_run, s_wsum,
-                                                             running, s_fe, s_carry, own);
+                                                             running);
     // refill stage (k+2) % 3 with tile t+2: its last user, tile t-1, was stored
     // from it; the producer warp waits until those bulk stores have read it (all
     // but its newest bulk group).  Plain loads/stores of tile t-1 from that stage
@@ -866,24 +791,6 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
       __syncwarp();
       if (lane == 0) fence_proxy_async_smem();
       issue(t + 2, (k + 2) % kStages);
-    }
-  }
-  if (a.carry) {
-    // the range's last partial sector of every bucket: [max(e & ~7, own), e)
-    __syncthreads();
-    auto flush = [&](uint32_t b, uint32_t e, uint32_t o) {
-      for (uint32_t p = max(e & ~7u, o); p < e; ++p) {
-        a.keys_out[p] = s_carry[b * 8u + (p & 7u)];
-        if constexpr (PAIRS) a.vals_out[p] = s_carry[m * 8u + b * 8u + (p & 7u)];
-      }
-    };
-    if constexpr (WSCAN) {
-      if (warp == 0) {
-        if (lane < m) flush(lane, running[0], own[0]);
-        if (lane + 32 < m) flush(lane + 32, running[1], own[1]);
-      }
-    } else if (tid < m) {
-      flush(tid, running[0], own[0]);
     }
   }
   if (a.store_runs) bulk_wait_all();  // run stores complete before smem is released

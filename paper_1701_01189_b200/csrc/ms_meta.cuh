@@ -57,8 +57,7 @@ template <int KIND, bool SMALLM, int ITEMS>
 __global__ void __launch_bounds__(kThreads + 32, 2)
     km_tile_meta(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
-                 uint32_t *__restrict__ R, uint32_t *__restrict__ hdr, uint32_t prefetch_ahead,
-                 uint32_t keep_last) {
+                 uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
   constexpr uint32_t W = kWarps;
   constexpr uint32_t SL = 32u * ITEMS;  // keys per warp slice
   constexpr uint32_t T = W * SL;
@@ -90,21 +89,13 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 
   if (warp == W) {
     // ============================ scan warp ===================================
-    auto prefetch = [&](uint32_t t) {  // beyond the ring: into L2 ahead of the TMA load
-      if (lane == 0 && t < t1 && via_tma(t))
-        prefetch_l2_bulk_hint(keys + (size_t)t * T, T * 4u, policy_evict_last());
-    };
     auto issue = [&](uint32_t t, uint32_t st) {
       if (lane == 0 && t < t1 && via_tma(t)) {
-        // the range's last keep_last tiles stay in L2 for KF, which starts there
-        const uint64_t pol = t + keep_last >= t1 ? policy_evict_last() : policy_evict_first();
         mbar_arrive_expect_tx(&full[st], T * 4u);
-        tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], pol);
+        tma_load_1d(km_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], policy_evict_first());
       }
-      prefetch(t + prefetch_ahead);
     };
     for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
-    for (uint32_t i = KS; i < KS + prefetch_ahead; ++i) prefetch(t0 + i);
     uint32_t running = 0;  // range count of bucket lane
     uint32_t k = 0;
     for (uint32_t t = t0; t < t1; ++t, ++k) {
@@ -189,40 +180,70 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 }
 
 // ============================================================================
-// Probe for kf_meta's RANK 8: one warp checks, over many bucket patterns, that
-// the values a shared-memory atomicAdd(p, 1) instruction returns to the lanes
-// that share an address are consecutive in lane order (what a stable rank
-// needs).  flag[0] = 1 if every pattern held.
+// Probe of reading R23: the old values that one warp-wide
+// shared-memory atomicAdd(p, 1) returns to the lanes sharing an address are
+// consecutive in lane order, and consecutive such instructions of a warp are
+// applied in program order.  Run in the postscan's own launch shape (512
+// threads, two CTAs per SM over the whole grid, every warp hammering its own
+// row of up to 256 counters with runs, random and skewed bucket patterns, 16
+// instructions back to back as in the rank loop); lane 0 of each warp replays
+// the same increments sequentially with plain loads and stores, and every
+// returned value must equal the replay.  *flag is cleared if any differs.
 // ============================================================================
-static __global__ void __launch_bounds__(32) k_probe_lane_ordered_inc(uint32_t *flag) {
-  __shared__ uint32_t ctr[32];
-  const uint32_t lane = threadIdx.x & 31u, lt = lanemask_lt();
+constexpr uint32_t kProbeWords = 1024u;  // per warp: row[256] | shadow[256] | bucket/expect[512]
+static __global__ void __launch_bounds__(kThreads, 2)
+    k_probe_lane_ordered_inc(uint32_t *flag, uint32_t patterns) {
+  extern __shared__ uint32_t pr_smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t *row = pr_smem + warp * kProbeWords, *shadow = row + 256, *ex = row + 512;
   bool ok = true;
-  for (uint32_t pat = 0; pat < 4096; ++pat) {
-    ctr[lane] = pat;  // arbitrary starting values
+  for (uint32_t pat = 0; pat < patterns; ++pat) {
+    const uint32_t salt = (blockIdx.x * 131u + warp) * 0x9E3779B9u + pat * 0x85EBCA6Bu;
+    const uint32_t mb = 1u + ((salt >> 7) & 255u);  // buckets in play: 1 .. 256
+    const uint32_t kind = pat & 3u;                  // random / runs / 90 % hot / two values
+    for (uint32_t j = lane; j < 256u; j += 32u) row[j] = shadow[j] = (salt ^ j) & 0xFFFFu;
+    uint32_t b[16], got[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      uint32_t h = salt ^ (lane * 0x2C1B3C6Du) ^ ((uint32_t)i * 0x297A2D39u);
+      h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+      uint32_t v = h % mb;
+      if (kind == 1u) v = ((lane + 32u * (uint32_t)i) * mb) >> 9;      // sorted runs
+      if (kind == 2u && (h >> 24) < 230u) v = salt % mb;               // 90 % one bucket
+      if (kind == 3u) v = (h >> 31) ? 0u : mb - 1u;                     // two buckets
+      b[i] = v;
+      ex[i * 32 + lane] = v;
+    }
     __syncwarp();
-    uint32_t h = (pat * 0x9E3779B9u) ^ (lane * 0x85EBCA6Bu);
-    h ^= h >> 15;
-    h *= 0x2C1B3C6Du;
-    h ^= h >> 12;
-    const uint32_t mb = 1u + (pat & 31u);  // buckets in play: 1 .. 32
-    const uint32_t b = (pat & 64u) ? (lane * mb) >> 5 : h % mb;  // runs or random
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
-    const uint32_t got = atomicAdd(ctr + b, 1u);
-    ok &= got == pat + (uint32_t)__popc(peers & lt);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) got[i] = atomicAdd(row + b[i], 1u);
+    __syncwarp();
+    if (lane == 0)
+      for (uint32_t e = 0; e < 512u; ++e) ex[e] = shadow[ex[e]]++;  // sequential replay
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) ok &= got[i] == ex[i * 32 + lane];
     __syncwarp();
   }
-  ok = __all_sync(0xFFFFFFFFu, ok);
-  if (lane == 0) flag[0] = ok ? 1u : 0u;
+  if (!__all_sync(0xFFFFFFFFu, ok) && lane == 0) atomicAnd(flag, 0u);
 }
 
 // Shared memory of kf_meta: 3 stages of [keys OS | values OS | meta MS] words,
-// peer masks [3][W][32], run tables [2][3][32] (or deltas [2][32]).
+// rank rows [3][W][32], run tables [3][3][32] (or deltas [3][32]).
 __host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
   const uint32_t T = kThreads * (pairs ? 8u : 16u);
   const size_t SW = (size_t)kf_out_slots(T, m) * (pairs ? 2u : 1u) + meta_stride(meta_ms(m), kWarps);
   return (3 * SW + 3 * kWarps * 32 + 3 * 3 * 32) * 4;
 }
+
+// Rank modes of kf_meta (m > 2; m <= 2 always ranks with one ballot per window):
+//   kRankInc   Eq.4 term 1 as the value a lane-ordered shared-memory increment
+//              of the warp's running slot returns (reading R23; used only on a
+//              device where the full-occupancy probe above passed);
+//   kRankMasks deterministic: peer masks by a shared-memory OR of the lane bit,
+//              taken and cleared by one atomic exchange per bucket lane, two
+//              windows in flight (Alg.3's peer masks).
+enum : int { kRankBallot = 0, kRankMasks = 7, kRankInc = 8 };
 
 // ============================================================================
 // KF (meta mode): persistent CTA per level-0 range, tiles in order; 16
@@ -235,27 +256,24 @@ __host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
 //   PROD (whole-run TMA bulk stores): the consumers arrive on placed[k % 3];
 //   the producer warp waits for it, issues tile t's run stores, and refills
 //   the stage of tile t-1 (read by now) with tile t+2 -- the consumers never
-//   wait for a store or issue one.
+//   wait for a store or issue one.  A tile that is not TMA-loaded (ragged last
+//   tile, unaligned input) is placed only after the producer has signalled
+//   empty[stage]: the bulk stores of the stage's previous tile have read it.
 //   !PROD: after the barrier the last warp issues tile t's run stores (TMA
 //   bulk) and every thread stores run heads / tails, or (no run stores) every
 //   thread scatters its slots; then the stage of tile t-1 gets tile t+2.
+// Meta records of tiles that are not TMA-loaded are read from global memory.
 // ============================================================================
-// RANK (m > 2): 0 = peer masks by shared-memory atomicOr of the lane bit;
-//               1 = peer masks from ceil(log2 m) ballots of the bucket bits
-//                   (Alg.3): no shared-memory traffic, more ALU work;
-//               2 / 3 = ballots for every third / every second window, atomics
-//                   for the others (balances the shared-memory and ALU pipes);
-//               4 / 5 / 6 = as 0 / 2 / 3 with the atomic windows' masks taken
-//                   and cleared by one atomic exchange per bucket lane;
-//               7 = as 4, two windows in flight at a time (full tiles).
 template <int KIND, bool PAIRS, bool SMALLM, int ITEMS, int RANK, bool PROD>
 __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(KfArgs a, BucketParams bp) {
   constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t kStages = 3;
+  constexpr uint32_t kPrefetch = 2;  // L2 prefetch distance beyond the ring (measured, profiles/r01)
   extern __shared__ __align__(128) uint8_t kf_smem[];
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ __align__(8) uint64_t placed[kStages];  // PROD: tile placed, 512 arrivals
+  __shared__ __align__(8) uint64_t empty[kStages];   // PROD: stage free for a non-TMA tile
   const uint32_t m = bp.m, mS = SMALLM ? 2u : m;
   const uint32_t OS = kf_out_slots(T, m);
   const uint32_t MS = meta_stride(mS, W);
@@ -269,15 +287,12 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   // the thread that issues the TMA loads: lane 0 of the producer warp (PROD) or
   // of the last consumer warp
   constexpr uint32_t kProducer = PROD ? NT : NT - 32;
-  const uint32_t logm = 32u - __clz(m - 1u);  // bucket bits (RANK 1)
 
   const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
   const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
   if (t0 >= t1) return;
-  // iteration k handles tile(k): forward, or (a.reverse) from the range's last
-  // tile down -- KM has just read the range's last tiles, still in L2
   const uint32_t nt = t1 - t0;
-  auto tile = [&](uint32_t k) { return k >= nt ? t1 : (a.reverse ? t1 - 1 - k : t0 + k); };
+  auto tile = [&](uint32_t k) { return k >= nt ? t1 : t0 + k; };
   auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
   auto via_tma = [&](uint32_t t) { return a.use_tma && tile_n(t) == T; };
   // one elected thread starts the TMA bulk copies of a tile: the input data
@@ -298,30 +313,28 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
                   policy_evict_first());
   };
   // the TMA ring holds only three tiles; tiles further ahead are prefetched
-  // into L2 so that their TMA loads later see L2 latency, not DRAM latency
+  // into L2 (evict_last, so that the streaming output does not evict them
+  // before their TMA load: measured +1-3.5 %)
   auto prefetch = [&](uint32_t t) {
     if (tid == kProducer && t < t1 && via_tma(t)) {
-      if (a.prefetch_keep) {
-        const uint64_t pol = policy_evict_last();
-        prefetch_l2_bulk_hint(a.keys_in + (size_t)t * T, T * 4u, pol);
-        if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)t * T, T * 4u, pol);
-        prefetch_l2_bulk_hint(a.meta + (size_t)t * MS, MS * 4u, pol);
-      } else {
-        prefetch_l2_bulk(a.keys_in + (size_t)t * T, T * 4u);
-        if constexpr (PAIRS) prefetch_l2_bulk(a.vals_in + (size_t)t * T, T * 4u);
-        prefetch_l2_bulk(a.meta + (size_t)t * MS, MS * 4u);
-      }
+      const uint64_t pol = policy_evict_last();
+      prefetch_l2_bulk_hint(a.keys_in + (size_t)t * T, T * 4u, pol);
+      if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)t * T, T * 4u, pol);
+      prefetch_l2_bulk_hint(a.meta + (size_t)t * MS, MS * 4u, pol);
     }
   };
   auto issue = [&](uint32_t k, uint32_t st) {
     issue_data(tile(k), st);
     issue_meta(tile(k), st);
-    prefetch(tile(k + a.prefetch_ahead));
+    prefetch(tile(k + kPrefetch));
   };
   if (tid == 0) {
     for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
     if constexpr (PROD)
-      for (uint32_t i = 0; i < kStages; ++i) mbar_init(&placed[i], NT);
+      for (uint32_t i = 0; i < kStages; ++i) {
+        mbar_init(&placed[i], NT);
+        mbar_init(&empty[i], 1);
+      }
   }
   __syncthreads();
   issue_data(tile(0), 0);
@@ -332,17 +345,19 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       griddep_wait();  // meta records are complete
       issue_meta(tile(0), 0);
       issue_meta(tile(1), 1);
-      for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(tile(j));
+      for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(tile(j));
       for (uint32_t k = 0; k < nt; ++k) {
         const uint32_t st = k % kStages;
         uint32_t *s_stage = stage0 + st * SW;
         const uint32_t *tab = s_tab + st * 96u;
         // refill the stage of tile t-1 with tile t+2 as soon as tile t-1's bulk
-        // stores have read it, before tile t's stores are queued behind it
+        // stores have read it, before tile t's stores are queued behind it; a
+        // tile that is not TMA-loaded gets the stage through empty[]
         bulk_wait_read();
         __syncwarp();
         if (lane == 0) fence_proxy_async_smem();
         issue(k + 2, (k + 2) % kStages);
+        if (lane == 0 && k + 2 < nt && !via_tma(tile(k + 2))) mbar_arrive(&empty[(k + 2) % kStages]);
         mbar_wait(&placed[st], (k / kStages) & 1u);
         // one TMA bulk store per bucket run body (16-byte aligned), then the
         // <= 3 leading / trailing elements of every run with plain stores
@@ -381,8 +396,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   }
 
   // keys (values) of one tile -> registers: lane l of warp w holds element
-  // w*32*ITEMS + 32 i + l.  TMA tiles come from the stage, others from global
-  // (and their meta record is copied into the stage by plain loads).
+  // w*32*ITEMS + 32 i + l.  TMA tiles come from the stage, others from global.
   uint32_t key[ITEMS];
   uint32_t val[PAIRS ? ITEMS : 1];
   const uint32_t wbase = warp * (ITEMS * 32);
@@ -406,7 +420,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         key[i] = e < tn ? __ldg(a.keys_in + g + e) : 0u;
         if constexpr (PAIRS) val[i] = e < tn ? __ldg(a.vals_in + g + e) : 0u;
       }
-      for (uint32_t i = tid; i < MS; i += NT) s[MO + i] = __ldg(a.meta + (size_t)t * MS + i);
     }
   };
 
@@ -418,7 +431,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   griddep_wait();  // KM complete: meta records and range histograms
   issue_meta(tile(0), 0);
   issue_meta(tile(1), 1);
-  for (uint32_t j = 2; j < 2 + a.prefetch_ahead; ++j) prefetch(tile(j));
+  for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(tile(j));
   uint32_t gbase = 0, grun = 0;
   {
     uint32_t *red = s_mask;  // [2][16][32] scratch (the mask rows are zeroed per tile)
@@ -459,7 +472,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     }
     if (lane < m) {
       gbase = incl - tot + pre;
-      if (a.reverse) grun = __ldg(a.R + (size_t)c * m + lane);  // the range's bucket total
       if (c == 0 && warp == 0 && a.bucket_offsets) {
         a.bucket_offsets[lane] = incl - tot;
         if (lane == m - 1) a.bucket_offsets[m] = incl;
@@ -469,13 +481,13 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   load_tile(tile(0), 0);
   named_barrier_sync(1, NT);
 
-  uint32_t *mrow0 = s_mask + warp * 32, *mrow1 = s_mask + (W + warp) * 32,
-           *mrow2 = s_mask + (2 * W + warp) * 32;
+  uint32_t *mrow0 = s_mask + warp * 32, *mrow1 = s_mask + (W + warp) * 32;
   for (uint32_t k = 0; k < nt; ++k) {
     const uint32_t t = tile(k);
     const uint32_t st = k % kStages;
     uint32_t *s_stage = stage0 + st * SW;
-    const uint32_t *rec = s_stage + MO;
+    const bool tma_tile = via_tma(t);
+    const uint32_t *rec = tma_tile ? s_stage + MO : a.meta + (size_t)t * MS;
     const uint32_t tn = tile_n(t);
     const bool full = tn == T;
     uint32_t *tab = s_tab + st * 96u;
@@ -488,11 +500,8 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       const uint32_t sbw = rec[warp * mS + lane];
       const uint32_t tb = rec[lane];
       const uint32_t te = lane + 1 < m ? rec[lane + 1] : tn;
-      // Eq.3 term 3: the range's tiles before this one (reverse: grun counts down
-      // from the range total)
-      if (a.reverse) grun -= te - tb;
-      const uint32_t gs = gbase + grun;
-      if (!a.reverse) grun += te - tb;
+      const uint32_t gs = gbase + grun;  // + Eq.3 term 3: the range's tiles before this one
+      grun += te - tb;
       const uint32_t adj = a.store_runs ? 4u * lane + ((gs - tb) & 3u) : 0u;
       wrun = sbw + adj;
       if (warp == W - 1) {
@@ -505,22 +514,22 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         }
       }
     }
-    if constexpr (!SMALLM && RANK != 1) {
+    if constexpr (!SMALLM && RANK == kRankMasks) {
       mrow0[lane] = 0u;
       mrow1[lane] = 0u;
-      mrow2[lane] = 0u;
     }
     __syncwarp();
+    if constexpr (PROD) {  // the stage's previous tile has been read by its bulk stores
+      if (!tma_tile && k >= 2) mbar_wait(&empty[st], a.use_tma ? 0u : ((k - 2) / kStages) & 1u);
+    }
 
     // ---- rank and place (Eq.4 term 1 + this warp's running slot) -------------
     bool derr = false;
     auto place = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
-      if constexpr (RANK == 8 && !SMALLM) {
+      if constexpr (RANK == kRankInc && !SMALLM) {
         // rank by the shared-memory atomic increment of this warp's running
-        // slot of the bucket: relies on same-address increments of one warp
-        // instruction being returned in lane order (checked bit-exactly by
-        // the parity tests; MS_META_RANK selects the other modes)
+        // slot of the bucket (reading R23)
         uint32_t *brow = mrow0;
         if (lane < m) brow[lane] = wrun;
         __syncwarp();
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         }
         return;
       }
-      if constexpr (RANK == 7 && FULL && !SMALLM && (ITEMS % 2 == 0)) {
+      if constexpr (RANK == kRankMasks && FULL && !SMALLM && (ITEMS % 2 == 0)) {
         // two windows at a time: both windows' shared-memory round trips
         // (OR of the lane bit, exchange of the bucket lane's mask) are in
         // flight together; only the cheap running-slot update is serial
@@ -594,52 +603,18 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
             c0 += __popc(vm) - nones;
           }
           c1 += nones;
-        } else if (RANK == 1 || ((RANK == 2 || RANK == 5) && i % 3 == 2) ||
-                   ((RANK == 3 || RANK == 6) && (i & 1))) {
-          // ballot voting on the bucket bits (Alg.3): lane j forms the mask of
-          // the lanes whose bucket is j (its own lane bits select vote or ~vote);
-          // a key with bucket b fetches lane b's mask and running slot
-          uint32_t mine = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
-#pragma unroll
-          for (uint32_t kb = 0; kb < 5; ++kb) {
-            if (kb < logm) {
-              const uint32_t v = __ballot_sync(0xFFFFFFFFu, (b >> kb) & 1u);
-              mine &= ((lane >> kb) & 1u) ? v : ~v;
-            }
-          }
-          const uint32_t peers = __shfl_sync(0xFFFFFFFFu, mine, b);
-          slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
-          wrun += __popc(mine);
-          if constexpr (RANK == 2 || RANK == 3) {  // mixed: keep the atomic windows' mask rotation
-            uint32_t *mprev = (i % 3 == 0) ? mrow2 : ((i % 3 == 1) ? mrow0 : mrow1);
-            __syncwarp();
-            if (i > 0 && lane < m) mprev[lane] = 0u;
-          }
-        } else if constexpr (RANK >= 4) {
-          // peer masks by one shared-memory OR of the lane bit; lane j takes
-          // bucket j's mask and clears it with one atomic exchange, the key of
-          // bucket b gets its peers and running slot from lane b by shuffles.
-          // Two rows alternate over the atomic windows, one __syncwarp each.
-          const int r = (RANK == 4 || RANK == 7) ? (i & 1) : (RANK == 5 ? (i % 3) : ((i >> 1) & 1));
-          uint32_t *mrow = r ? mrow1 : mrow0;
+        } else {
+          // one window at a time (partial tiles of kRankMasks): peer masks by
+          // one shared-memory OR of the lane bit; lane j takes bucket j's mask
+          // and clears it with one atomic exchange, the key of bucket b gets
+          // its peers and running slot from lane b by shuffles.  Two rows
+          // alternate, one __syncwarp each.
+          uint32_t *mrow = (i & 1) ? mrow1 : mrow0;
           if (valid) atomicOr(mrow + b, lanebit);
           __syncwarp();
           const uint32_t mine = atomicExch(mrow + lane, 0u);  // lanes >= m: an unused, zero word
           const uint32_t peers = __shfl_sync(0xFFFFFFFFu, mine, b);
           slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
-          wrun += __popc(mine);
-        } else {
-          // peer masks by one shared-memory OR of the lane bit (Alg.3's ballot
-          // voting in one instruction); lane j keeps bucket j's running slot;
-          // three mask rows rotate so one __syncwarp per window suffices
-          uint32_t *mrow = (i % 3 == 0) ? mrow0 : ((i % 3 == 1) ? mrow1 : mrow2);
-          uint32_t *mprev = (i % 3 == 0) ? mrow2 : ((i % 3 == 1) ? mrow0 : mrow1);
-          if (valid) atomicOr(mrow + b, lanebit);
-          __syncwarp();
-          const uint32_t peers = valid ? mrow[b] : 0u;
-          const uint32_t mine = lane < m ? mrow[lane] : 0u;
-          slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
-          if (i > 0 && lane < m) mprev[lane] = 0u;
           wrun += __popc(mine);
         }
         if (valid) {

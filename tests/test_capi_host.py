@@ -121,3 +121,25 @@ def test_no_cpu_fallback_in_product_path():
     import paper_1701_01189_b200 as ms
     src = open(ms.__file__).read() + open(_lib.__file__).read()
     assert "oracle" not in src.replace("no CPU fallback", "")
+
+
+def test_options_host(lib):
+    """ms_set_option / ms_get_option are host-only: defaults, validation, round trip."""
+    assert lib.ms_get_option(_lib.MS_OPT_RANK) == _lib.MS_RANK_AUTO
+    assert lib.ms_get_option(_lib.MS_OPT_RUN_STORES) == 1
+    assert lib.ms_get_option(_lib.MS_OPT_PIPELINE) == _lib.MS_PIPELINE_LEVEL0
+    assert lib.ms_get_option(3) == -1
+    assert lib.ms_set_option(_lib.MS_OPT_RANK, 5) == _lib.MS_ERR_INVALID_VALUE
+    assert lib.ms_set_option(9, 0) == _lib.MS_ERR_INVALID_VALUE
+    assert lib.ms_set_option(_lib.MS_OPT_RANK, _lib.MS_RANK_PEER_MASKS) == 0
+    assert lib.ms_get_option(_lib.MS_OPT_RANK) == _lib.MS_RANK_PEER_MASKS
+    assert lib.ms_set_option(_lib.MS_OPT_RANK, _lib.MS_RANK_AUTO) == 0
+
+
+def test_workspace_alignment_rejected(lib):
+    """A workspace that is not 256-byte aligned is rejected before any launch."""
+    fn = _lib.ms_bucket_fn(_lib.MS_BUCKET_DELTA, 4, 1 << 30, 0, 0)
+    st = lib.ms_multisplit_keys(0x1000, 0x2000, 0, ctypes.byref(fn), None, 0x10010, 1 << 20, None)
+    assert st == _lib.MS_ERR_INVALID_VALUE
+    st = lib.ms_radix_sort_keys(0x1000, 0x2000, 10, 0, 32, 8, 0x10004, 1 << 30, None)
+    assert st == _lib.MS_ERR_INVALID_VALUE

@@ -58,10 +58,12 @@ def test_c3_pairs_2p27(m, kind, dist):
     assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev) and np.array_equal(host(off), eo)
 
 
-def test_c4_radix_sort_pairs_2p28():
+@pytest.mark.parametrize("r", [8, 0])
+def test_c4_radix_sort_pairs_2p28(r):
+    """configs[3] as benched (r = 8: 4 x 8-bit passes over [0, 32)) and the library default."""
     n = 1 << 28
     k, v = gen_dev(n, 0x5EED)
-    ko, vo = ms.radix_sort(k, v)
+    ko, vo = ms.radix_sort(k, v, begin_bit=0, end_bit=32, bits_per_pass=r)
     kh = host(k)
     ok, ov = host(ko), host(vo)
     assert np.all(ok[1:] >= ok[:-1])                       # sorted
@@ -76,8 +78,8 @@ def test_c4_radix_sort_pairs_2p28():
     for i in rng.integers(0, n, 64):
         assert ok[i] == ks[i]
     del ks
-    ko2, _ = ms.radix_sort(k)
+    ko2, _ = ms.radix_sort(k, bits_per_pass=r)
     assert torch.equal(ko2, ko)
     small_k, small_v = oracle.radix_sort(kh[:1 << 20], np.arange(1 << 20, dtype=np.uint32))
-    ko3, vo3 = ms.radix_sort(k[:1 << 20].clone(), v[:1 << 20].clone())
+    ko3, vo3 = ms.radix_sort(k[:1 << 20].clone(), v[:1 << 20].clone(), bits_per_pass=r)
     assert np.array_equal(host(ko3), small_k) and np.array_equal(host(vo3), small_v)

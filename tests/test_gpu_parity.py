@@ -141,14 +141,88 @@ def test_unaligned_outputs(m):
     assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev)
 
 
-def test_per_element_store_path(monkeypatch):
-    monkeypatch.setenv("MS_NO_RUN_STORES", "1")
+@pytest.fixture
+def option():
+    """Set libms options for one test and restore the defaults afterwards."""
+    lib = ms._lib
+    saved = {o: ms.get_option(o) for o in (lib.MS_OPT_RANK, lib.MS_OPT_RUN_STORES, lib.MS_OPT_PIPELINE)}
+    yield ms.set_option
+    for o, v in saved.items():
+        ms.set_option(o, v)
+
+
+def test_per_element_store_path(option):
+    option(ms._lib.MS_OPT_RUN_STORES, 0)
     for m in (2, 32):
         ob, pb, gk = bucket_pair("delta", m)
         n = 7 * T + 5
         keys = gen.keys(n, seed=m, dist=gen.DIST_BINOMIAL, **gk)
         check_multisplit(keys, gen.values(n, seed=1), ob, pb)
         check_multisplit(keys, None, ob, pb)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+@pytest.mark.parametrize("m", [3, 16, 32, 64, 128, 256])
+def test_deterministic_rank_mode(option, m, pairs):
+    """MS_RANK_PEER_MASKS (no reliance on reading R23) gives the same bit-exact result."""
+    option(ms._lib.MS_OPT_RANK, ms._lib.MS_RANK_PEER_MASKS)
+    ob, pb, gk = bucket_pair("delta", m)
+    for n, dist in ((5 * T + 77, gen.DIST_UNIFORM), (3 * T + 1, gen.DIST_SKEW)):
+        keys = gen.keys(n, seed=m + n, dist=dist, **gk)
+        check_multisplit(keys, gen.values(n, seed=4) if pairs else None, ob, pb)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+def test_unaligned_inputs_many_tiles_producer_warp(pairs):
+    """Unaligned input (no TMA loads) with aligned outputs, m <= 16 (producer-warp
+    run stores), enough tiles per CTA range to lap the three-stage ring, ragged tail
+    (the producer/consumer stage hand-off for non-TMA tiles)."""
+    for m in (4, 16):
+        ob, pb, gk = bucket_pair("delta", m)
+        n = (1 << 24) + 4099
+        keys = gen.keys(n + 1, seed=m, **gk)
+        vals = gen.values(n + 1, seed=m) if pairs else None
+        kd = dev(keys)[1:]
+        vd = dev(vals)[1:] if pairs else None
+        ko, vo, off = ms.multisplit(kd, vd, bucket=pb)
+        ek, ev, eo = oracle.multisplit(keys[1:], ob, vals[1:] if pairs else None)
+        assert np.array_equal(host(ko), ek)
+        if pairs:
+            assert np.array_equal(host(vo), ev)
+        assert np.array_equal(host(off), eo)
+
+
+def test_c1_exact():
+    """BASELINE configs[0]: n = 2^10 uniform keys, m = 2 delta buckets (single-CTA path)."""
+    ob, pb, gk = bucket_pair("delta", 2)
+    for seed in (1, 2, 3):
+        keys = gen.keys(1 << 10, seed=seed, **gk)
+        check_multisplit(keys, None, ob, pb)
+        check_multisplit(keys, gen.values(1 << 10, seed=seed), ob, pb)
+
+
+@pytest.mark.parametrize("m", [2, 4, 8, 16, 32, 64, 128, 256])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_sweep_m_multi_tile(m, pairs):
+    """Every m of the bench sweep (delta buckets, Delta = ceil(2^32/m)) over many tiles."""
+    ob, pb, gk = bucket_pair("delta", m)
+    n = 37 * T + 1234
+    keys = gen.keys(n, seed=100 + m, **gk)
+    check_multisplit(keys, gen.values(n, seed=m) if pairs else None, ob, pb)
+
+
+@pytest.mark.parametrize("m", [64, 128, 256])
+@pytest.mark.parametrize("dist", [gen.DIST_UNIFORM, gen.DIST_SKEW])
+def test_c3_radix_and_identity(m, dist):
+    """configs[2] bucket kinds (identity, radix digit) at m = 64/128/256, uniform and 90 % skew."""
+    for kind in ("identity", "radix"):
+        ob, pb, gk = bucket_pair(kind, m)
+        if kind == "radix":  # the bench's C3 radix digit: the low bits
+            bits = m.bit_length() - 1
+            ob, pb, gk = oracle.radix(0, bits), ms.Radix(0, bits), dict(kind=gen.RADIX, m=m, shift=0, bits=bits)
+        n = 45 * 4096 + 3
+        keys = gen.keys(n, seed=m, dist=dist, alpha=0.1, **gk)
+        check_multisplit(keys, gen.values(n, seed=5), ob, pb)
 
 
 def test_custom_delta_widths():
@@ -199,12 +273,14 @@ def test_stage_scan(shape):
 
 @pytest.mark.parametrize("n", [0, 1, 1000, T, 4 * T + 9, 1 << 20])
 @pytest.mark.parametrize("pairs", [False, True])
-def test_radix_sort(n, pairs):
+@pytest.mark.parametrize("r", [0, 8])
+def test_radix_sort(n, pairs, r):
+    """r = 8: the benched configs[3] schedule, 4 x 8-bit passes over [0, 32); r = 0: the default."""
     keys = gen.keys(n, seed=9)
     keys[::5] &= np.uint32(0xFF00FF)  # duplicates make stability visible
     vals = gen.values(n, seed=9)
     ek, ev = oracle.radix_sort(keys, vals if pairs else None)
-    ko, vo = ms.radix_sort(dev(keys), dev(vals) if pairs else None)
+    ko, vo = ms.radix_sort(dev(keys), dev(vals) if pairs else None, begin_bit=0, end_bit=32, bits_per_pass=r)
     assert np.array_equal(host(ko), ek)
     if pairs:
         assert np.array_equal(host(vo), ev)
@@ -223,9 +299,9 @@ def test_radix_sort_bits(args):
 
 @pytest.mark.parametrize("pairs", [False, True])
 @pytest.mark.parametrize("m", [2, 37, 256])
-def test_three_launch_mode(monkeypatch, pairs, m):
-    # MS_PIPELINE=3pass: the paper's {tile histograms H, scan of H, postscan}
-    monkeypatch.setenv("MS_PIPELINE", "3pass")
+def test_three_launch_mode(option, pairs, m):
+    # MS_PIPELINE_TILE: the paper's {tile histograms H, scan of H, postscan}
+    option(ms._lib.MS_OPT_PIPELINE, ms._lib.MS_PIPELINE_TILE)
     ob, pb, gk = bucket_pair("delta", m)
     n = 29 * T + 333
     keys = gen.keys(n, seed=m, dist=gen.DIST_SKEW, **gk)

@@ -1,38 +1,66 @@
-"""Every rank mode of the m <= 32 postscan (kf_meta RANK, ms_meta.cuh) and both
-store structures (producer warp or not) are bit-exact against the oracle; and
-the hardware property the default mode relies on (lane-ordered shared-memory
-increments, probed by ms_lane_ordered_increment) holds on this GPU."""
-import os
-import subprocess
-import sys
-
+"""The hardware property the default rank relies on (reading R23: lane-ordered
+shared-memory increments, probed by ms_device_init over the whole grid in the
+postscan's launch shape) holds on this GPU; and every pipeline option of the
+library (deterministic peer-mask ranking, per-element stores, the paper's
+three-launch pipeline) is bit-exact against the oracle on multi-tile inputs
+with ragged tails, several m <= 32 and skewed bucket distributions."""
+import numpy as np
 import pytest
+import torch
+
+import oracle
+from gen import inputs as gen
 
 pytestmark = pytest.mark.gpu
-
-HERE = os.path.dirname(os.path.abspath(__file__))
+ms = pytest.importorskip("paper_1701_01189_b200")
 
 
 def test_lane_ordered_increment_probe():
-    ms = pytest.importorskip("paper_1701_01189_b200")
+    ms.device_init(0)
     assert ms._lib.load().ms_lane_ordered_increment() == 1
 
 
-@pytest.mark.parametrize("rank", ["atomic", "ballot", "mix3", "mix2", "xatomic", "xmix3", "xmix2", "xpair", "inc"])
-@pytest.mark.parametrize("prod", ["0", "1"])
-def test_rank_mode_parity(rank, prod):
-    env = dict(os.environ, MS_META_RANK=rank, MS_META_PROD=prod)
-    r = subprocess.run([sys.executable, os.path.join(HERE, "_rank_mode_check.py")], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+def test_options_api():
+    lib = ms._lib
+    assert ms.get_option(lib.MS_OPT_RANK) in (0, 1)
+    with pytest.raises(ms.MultisplitError):
+        ms.set_option(lib.MS_OPT_RANK, 7)
+    with pytest.raises(ms.MultisplitError):
+        ms.set_option(99, 0)
+    assert ms.get_option(99) == -1
 
 
-@pytest.mark.parametrize("env", [{"MS_KF_REVERSE": "1", "MS_KM_KEEP": "4"}, {"MS_KF_PREFETCH": "0"},
-                                 {"MS_KM_PREFETCH": "2"}, {"MS_NO_META": "1"}, {"MS_NO_RANK_INC": "1"},
-                                 {"MS_NO_RUN_STORES": "1"}])
-def test_pipeline_options_parity(env):
-    """Measured-and-rejected or fallback pipeline options stay bit-exact."""
-    e = dict(os.environ, **env)
-    r = subprocess.run([sys.executable, os.path.join(HERE, "_rank_mode_check.py")], env=e,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+CASES = []
+for m in (3, 5, 8, 13, 16, 17, 32, 33, 100, 256):
+    for n, pairs, dist in ((3 * 8192 + 77, False, gen.DIST_UNIFORM), (5 * 4096 + 1, True, gen.DIST_UNIFORM),
+                           (40000, False, gen.DIST_SKEW), (9000, True, gen.DIST_BINOMIAL)):
+        CASES.append((m, n, pairs, dist))
+
+OPTIONS = {"default": {}, "peer_masks": {0: 1}, "no_run_stores": {1: 0}, "tile_pipeline": {2: 1},
+           "peer_masks_no_run_stores": {0: 1, 1: 0}}
+
+
+@pytest.mark.parametrize("opts", sorted(OPTIONS))
+def test_option_parity(opts):
+    saved = {o: ms.get_option(o) for o in (0, 1, 2)}
+    try:
+        for o, v in OPTIONS[opts].items():
+            ms.set_option(o, v)
+        bad = []
+        for m, n, pairs, dist in CASES:
+            ob = oracle.delta(m)
+            k = gen.keys(n, seed=m * 7 + n, kind=gen.DELTA, m=m, delta=ob.delta, dist=dist, alpha=0.1)
+            v = gen.values(n, seed=3) if pairs else None
+            ek, ev, eo = oracle.multisplit(k, ob, v)
+            kd = torch.from_numpy(k.view(np.int32)).cuda()
+            vd = torch.from_numpy(v.view(np.int32)).cuda() if pairs else None
+            ko, vo, off = ms.multisplit(kd, vd, bucket=ms.Delta(m))
+            ok = np.array_equal(ko.cpu().numpy().view(np.uint32), ek) and \
+                np.array_equal(off.cpu().numpy().view(np.uint32), eo) and \
+                (not pairs or np.array_equal(vo.cpu().numpy().view(np.uint32), ev))
+            if not ok:
+                bad.append((m, n, pairs, dist))
+        assert not bad, bad
+    finally:
+        for o, v in saved.items():
+            ms.set_option(o, v)
