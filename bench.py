@@ -31,6 +31,14 @@ sys.path.insert(0, ROOT)
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+NOMINAL_HBM_GBS = 8000.0   # nominal B200 HBM3e (context: SURVEY 8(d) asks for both fractions)
+
+
+def kernel_name(m: int) -> str:
+    """The postscan kernel (dominant kernel) of the pipeline libms picks for m."""
+    if m <= 32:
+        return "kf_meta (KF: rank + in-place reorder + coalesced / run stores; prescan KM)"
+    return "kf_meta_wide (KF: packed-increment rank + in-place reorder + coalesced stores; prescan KMW, scan KR)"
 
 # workload -> (n, pairs, kind, default m, metric unit, algorithmic bytes per element)
 # Algorithmic bytes: the paper's speed-of-light accounting (P:1367-1371): keys are
@@ -44,6 +52,12 @@ WORKLOADS = {
                         desc="key-value multisplit, n=2^27, identity buckets (configs[2])"),
     "ms_pairs_c3_skew": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
                              dist="skew", desc="key-value multisplit, n=2^27, identity, 90% one bucket (configs[2])"),
+    "ms_pairs_c3_radix": dict(n=1 << 27, pairs=True, kind="radix", m=256, unit="Gpairs/s", bpe=20,
+                              desc="key-value multisplit, n=2^27, radix-digit buckets (low bits) (configs[2])"),
+    "ms_pairs_c3_radix_skew": dict(n=1 << 27, pairs=True, kind="radix", m=256, unit="Gpairs/s", bpe=20,
+                                   dist="skew", desc="key-value multisplit, n=2^27, radix digits, 90% one bucket"),
+    "ms_keys_c1": dict(n=1 << 10, pairs=False, kind="delta", m=2, unit="Gkeys/s", bpe=12,
+                       desc="key-only multisplit, n=2^10 uniform uint32, m=2 delta buckets (configs[0])"),
     "ms_sharded_c5": dict(n=1 << 30, pairs=True, kind="delta", m=256, unit="Gpairs/s", bpe=20,
                           desc="sharded key-value multisplit, n=2^30 pairs in total over the ranks, m=256 "
                                "delta buckets (configs[4]); n is per job, split evenly", strong=True),
@@ -186,15 +200,23 @@ class Runner:
         self.off = torch.empty(m + 1, dtype=torch.int32, device=dev)
         if kind == "sort":
             self.ws = torch.empty(ms.radix_sort_workspace_size(n, wl["pairs"]), dtype=torch.uint8, device=dev)
+        elif world > 1:
+            from paper_1701_01189_b200 import sharded
+            self.comm = sharded.Comm()
+            self.comm.register_output(self.ko, self.vo)
+            self.ws = torch.empty(max(1, self.comm.workspace_size(n, m, wl["pairs"])), dtype=torch.uint8,
+                                  device=dev)
         else:
             self.ws = torch.empty(max(1, ms.workspace_size(n, m, wl["pairs"])), dtype=torch.uint8, device=dev)
+        ms.device_init(dev.index)
 
     def step(self, keys=None, ko=None):
         keys = self.keys if keys is None else keys
         ko = self.ko if ko is None else ko
-        if self.world > 1:
+        if self.world > 1:  # the library's sharded call (fused KP path: registered windows)
             from paper_1701_01189_b200 import sharded
-            self.ko, self.vo, _ = sharded.sharded_multisplit(keys, self.vals, self.bucket)
+            sharded.multisplit(self.comm, keys, self.vals, bucket=self.bucket, out_keys=ko,
+                               out_values=self.vo, workspace=self.ws)
             return
         if self.wl["kind"] == "hist_even":
             self.ms.histogram_even(self.samples, self.m, 0.0, 1024.0, out=self.counts)
@@ -361,16 +383,14 @@ def run_ours(args, rank, world, local_rank):
     elif stages is not None:
         ks_bytes = n * (16 if wl["pairs"] else 8)
         achieved = ks_bytes / (stages["postscan"] * 1e-3) / 1e9
-        # m <= 32: KM (prescan + per-(tile, warp) slot bases) -> KF kf_meta; otherwise
-        # KU -> KR -> KF kf_fused
-        kname = ("kf_meta (KF: rank + in-place reorder + run stores)" if m <= 32 and wl["kind"] != "sort"
-                 else "kf_fused (KF: count + scan + rank + reorder + scatter)")
+        kname = kernel_name(m if wl["kind"] != "sort" else 1 << wl.get("bits", 8))
         roofline = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1),
                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                     "traffic": load_traffic(f"{args.workload}_m{m}"),
                     "alg_bytes_per_launch": ks_bytes, "peak_source": peak_src,
                     "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
     whole_frac = value * 1e9 / world * wl["bpe"] / (hbm * 1e9)
+    nominal_frac = value * 1e9 / world * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9)
     e2e_ms, h2d, d2h = e2e_steps(run, max(3, args.steps // 4), 2)
     out = {
         "metric": (f"histogram {wl['unit']} ({args.workload}, m={m})" if wl["kind"].startswith("hist") else
@@ -382,8 +402,10 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (seeded counter-based generator)",
         "config": {"workload": wl["desc"], "n_per_rank": n, "n_total": n * world, "m": m, "bucket": wl["kind"],
                    "pairs": wl["pairs"], "l2": "flushed before every timed step (512 MiB write)",
-                   "parallelism": f"sharded{world} (NCCL all-gather + all-to-all-v)" if world > 1 else "single"},
+                   "parallelism": (f"sharded{world} (libms: NCCL all-gather of counts + fused NVLink peer-store "
+                                   f"scatter KP)" if world > 1 else "single")},
         "hbm_roofline_frac_whole_op": round(whole_frac, 4),
+        "hbm_roofline_frac_whole_op_nominal_8tbs": round(nominal_frac, 4),
         "roofline": roofline,
         "e2e": {"value": round(n * world / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl["unit"],
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -394,6 +416,7 @@ def run_ours(args, rank, world, local_rank):
         out["sweep"] = sweep(args, dev, flush, hbm)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, m)
+        out["cpu_parallel"] = cpu_parallel(wl, m)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -401,13 +424,18 @@ def run_ours(args, rank, world, local_rank):
 
 
 def sweep(args, dev, flush, hbm):
-    """Per-m throughput table (BASELINE.md §2 layout), a few steps each."""
+    """Per-m throughput table (BASELINE.md section 2 layout), a few steps each: keys and
+    pairs at every m of the metric (2..256, configs[1] size), configs[2] identity and
+    radix digits (uniform and 90 % skew), configs[3] sorts, configs[0] latency, f2."""
     import torch
     res = {}
-    cases = [("ms_keys", m) for m in (2, 8, 32, 64, 256)] + [("ms_pairs", m) for m in (2, 8, 32, 256)] + \
-            [("ms_pairs_c3", 64), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256), ("sort_keys", 256),
-             ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32), ("hist_even", 2),
-             ("hist_even", 256), ("hist_range", 2), ("hist_range", 256)]
+    cases = [("ms_keys", m) for m in (2, 4, 8, 16, 32, 64, 128, 256)] + \
+            [("ms_pairs", m) for m in (2, 4, 8, 16, 32, 64, 128, 256)] + \
+            [("ms_pairs_c3", 64), ("ms_pairs_c3", 128), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256),
+             ("ms_pairs_c3_radix", 64), ("ms_pairs_c3_radix", 128), ("ms_pairs_c3_radix", 256),
+             ("ms_pairs_c3_radix_skew", 256),
+             ("sort_keys", 256), ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32),
+             ("hist_even", 2), ("hist_even", 256), ("hist_range", 2), ("hist_range", 256)]
     for name, m in cases:
         wl = WORKLOADS[name]
         run = Runner(wl, m, dev)
@@ -417,13 +445,72 @@ def sweep(args, dev, flush, hbm):
         t = sum(times) / len(times)
         rate = wl["n"] / (t * 1e-3) / 1e9
         e = {"value": round(rate, 2), "unit": wl["unit"], "ms": round(t, 4),
-             "hbm_frac": round(rate * 1e9 * wl["bpe"] / (hbm * 1e9), 3)}
+             "hbm_frac": round(rate * 1e9 * wl["bpe"] / (hbm * 1e9), 3),
+             "hbm_frac_nominal": round(rate * 1e9 * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9), 3)}
         if stages:
             e["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
+            e["kf_frac"] = round(wl["n"] * (16 if wl["pairs"] else 8) / (stages["postscan"] * 1e-3) / 1e9 / hbm, 3)
         res[f"{name}_m{m}"] = e
         del run
         torch.cuda.empty_cache()
+    res["c1_latency"] = c1_latency(dev)
     return res
+
+
+def c1_latency(dev):
+    """configs[0]: n = 2^10 keys, m = 2 delta buckets -- microseconds per call through the
+    public API (one launch, latency-bound), back to back and replayed from a CUDA graph,
+    next to the CPU stable counting sort (the oracle) on the same keys."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_1701_01189_b200 as ms
+    from gen import inputs as gen
+    n, m = 1 << 10, 2
+    fn = oracle.delta(m)
+    kh = gen.keys(n, SEED, kind=gen.DELTA, m=m, delta=fn.delta)
+    k = torch.from_numpy(kh.view(np.int32)).to(dev)
+    ko = torch.empty_like(k)
+    off = torch.empty(m + 1, dtype=torch.int32, device=dev)
+    ws = torch.empty(max(1, ms.workspace_size(n, m, False)), dtype=torch.uint8, device=dev)
+    b = ms.Delta(m)
+    call = lambda: ms.multisplit(k, None, bucket=b, out_keys=ko, out_offsets=off, workspace=ws)  # noqa: E731
+    for _ in range(20):
+        call()
+    torch.cuda.synchronize()
+    reps = 2000
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    us_call = e0.elapsed_time(e1) * 1e3 / reps
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        call()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(10):
+            call()
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps // 10):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us_graph = e0.elapsed_time(e1) * 1e3 / reps
+    ok = np.array_equal(ko.cpu().numpy().view(np.uint32), oracle.multisplit(kh, fn)[0])
+    t0 = time.perf_counter()
+    for _ in range(200):
+        oracle.multisplit(kh, fn)
+    us_cpu = (time.perf_counter() - t0) * 1e6 / 200
+    return {"unit": "us/call", "gpu_us_per_call": round(us_call, 3), "gpu_us_per_call_cuda_graph": round(us_graph, 3),
+            "cpu_oracle_us_per_call": round(us_cpu, 3), "parity": bool(ok),
+            "note": "n=2^10, m=2; the oracle time includes the ctypes call from Python"}
 
 
 # --------------------------------------------------------------------------- oracle (CPU) arm
@@ -470,6 +557,43 @@ def cpu_baseline(wl, m, budget_s: float = 12.0):
             "host_cores_available": len(os.sched_getaffinity(0))}
 
 
+def cpu_parallel(wl, m, budget_s: float = 6.0):
+    """The paper's {local, global, local} multisplit on ALL host cores (baseline/, C with
+    pthreads) on a bounded sample of the workload: context for the GPU rate."""
+    import numpy as np
+    import baseline
+    import oracle
+    from gen import inputs as gen
+    cores = len(os.sched_getaffinity(0))
+    kind = wl["kind"]
+    n_sample = min(wl["n"], 1 << 25)
+    if kind.startswith("hist"):
+        return None
+    if kind == "sort":
+        k = gen.keys(n_sample, SEED)
+        v = gen.values(n_sample, SEED, parity=False) if wl["pairs"] else None
+        f = lambda: baseline.radix_sort(k, v, wl.get("bits", 8), cores)  # noqa: E731
+    else:
+        if kind == "delta":
+            fn = oracle.delta(m)
+            k = gen.keys(n_sample, SEED, kind=gen.DELTA, m=m, delta=fn.delta)
+            kw = dict(delta=fn.delta)
+        else:  # identity / radix: digits of the low bits
+            bits = max(1, (m - 1).bit_length())
+            k = gen.keys(n_sample, SEED, kind=gen.RADIX, m=1 << bits, shift=0, bits=bits)
+            kw = dict(bits=bits)
+        v = gen.values(n_sample, SEED, parity=False) if wl["pairs"] else None
+        f = lambda: baseline.multisplit(k, v, m if kind == "delta" else 1 << kw.get("bits", 1), threads=cores, **kw)  # noqa: E731
+    f()
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        f()
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(n_sample / dt / 1e9, 4), "unit": wl["unit"], "cores": cores, "kind": "parallel C (pthreads)",
+            "sample": f"{reps} x {n_sample} elements of the same workload (seed {SEED})"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -513,8 +637,17 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # not under torchrun: launch N ranks (one process per GPU) ourselves
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -42,7 +42,7 @@ typedef enum {
   MS_ERR_WORKSPACE = 3,     /* ws_bytes smaller than the *_workspace_size value */
   MS_ERR_CUDA = 4,          /* a CUDA launch / runtime error */
   MS_ERR_KEY_DOMAIN = 5,    /* device-detected: identity key >= m */
-  MS_ERR_NCCL = 6           /* reserved for the sharded path */
+  MS_ERR_NCCL = 6           /* NCCL missing or an NCCL call failed (sharded calls) */
 } ms_status;
 
 /* Bucket identifiers f(u). */
@@ -260,6 +260,85 @@ ms_status ms_shard_merge_pairs(const uint32_t *keys_recv, const uint32_t *vals_r
                                uint64_t n_recv, const ms_bucket_fn *fn,
                                const uint32_t *recv_starts, const uint32_t *merge_offsets,
                                uint32_t G, uint32_t *keys_out, uint32_t *vals_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Sharded multisplit as the library's own call (Eq.(3), with the
+ * G ranks of one node as the first level of localization).  One process per
+ * GPU; rank s holds input shard s (n_s elements, global indices N_<s ..
+ * N_<s + n_s - 1 of the rank-order concatenation) and receives output shard s
+ * (the same global index range of the stable multisplit of that
+ * concatenation, so n_s elements too).  sum_s n_s must be < 2^32.
+ *
+ * NCCL is bound at run time (dlopen of libnccl.so.2: the process's copy, e.g.
+ * PyTorch's); without it every call below returns MS_ERR_NCCL.
+ *
+ *   ms_comm_unique_id  rank 0 only: 128 opaque bytes the caller broadcasts
+ *                      (e.g. over a torch.distributed process group).
+ *   ms_comm_init       collective over the G ranks (G <= 8): binds the
+ *                      current process to `cuda_device` and creates the NCCL
+ *                      communicator.  ms_comm_destroy releases everything.
+ *   ms_comm_register_output
+ *                      collective, synchronous: registers this rank's output
+ *                      buffers (n_local words each; vals_out may be NULL) as
+ *                      windows the other ranks map through CUDA IPC (buffers
+ *                      from cudaMalloc or a caching allocator on top of it).
+ *   ms_multisplit_{keys,pairs}_sharded
+ *                      collective, stream-ordered on `stream`.  When keys_out
+ *                      (and vals_out) are the registered windows and n_local
+ *                      their size, the fused path KP runs: local prescan ->
+ *                      NCCL all-gather of the G x m bucket counts -> plan
+ *                      kernel (Eq.3 terms 1-2 per bucket) -> postscan that
+ *                      stores every element straight into the window of the
+ *                      rank owning its global position (NVLink peer stores;
+ *                      no staging, no merge, no host synchronization) -> an
+ *                      NCCL all-reduce of one word as the completion barrier.
+ *                      Otherwise the NCCL path runs: local multisplit into the
+ *                      workspace -> all-gather of the offsets -> one D2H copy +
+ *                      stream synchronization -> host plan (ms_shard_plan) ->
+ *                      ncclSend / ncclRecv of contiguous ranges -> KX merge.
+ *                      KP needs m <= 32, or the device's lane-order probe
+ *                      (ms_device_init) for m > 32; else the NCCL path runs.
+ *                      global_bucket_offsets: NULL or m+1 device uint64 words
+ *                      (start of each bucket in the global output, [m] = n_total).
+ *   ms_sharded_workspace_size: bytes of `ws` (256-byte aligned) for either path.
+ * --------------------------------------------------------------------- */
+typedef struct ms_comm ms_comm;
+ms_status ms_comm_unique_id(void *out128);
+ms_status ms_comm_init(ms_comm **comm, int nranks, int rank, const void *id128, int cuda_device);
+ms_status ms_comm_destroy(ms_comm *comm);
+ms_status ms_comm_register_output(ms_comm *comm, uint32_t *keys_out, uint32_t *vals_out,
+                                  uint64_t n_local);
+size_t ms_sharded_workspace_size(const ms_comm *comm, uint64_t n_local, uint32_t m, int with_values);
+ms_status ms_multisplit_keys_sharded(ms_comm *comm, const uint32_t *keys_in, uint32_t *keys_out,
+                                     uint64_t n_local, const ms_bucket_fn *fn,
+                                     uint64_t *global_bucket_offsets, void *ws, size_t ws_bytes,
+                                     void *stream);
+ms_status ms_multisplit_pairs_sharded(ms_comm *comm, const uint32_t *keys_in, const uint32_t *vals_in,
+                                      uint32_t *keys_out, uint32_t *vals_out, uint64_t n_local,
+                                      const ms_bucket_fn *fn, uint64_t *global_bucket_offsets,
+                                      void *ws, size_t ws_bytes, void *stream);
+
+/* The two steps of the fused path KP without the collectives, so that G
+ * "virtual ranks" can run on one GPU (the collectives become copies):
+ *   ms_shard_prescan: prescan of this rank's shard into `ws` (which must then
+ *     be passed unchanged to ms_shard_scatter); counts (m device words, may be
+ *     NULL) receives the shard's bucket counts C[r][0..m).
+ *   ms_shard_scatter: C = the G x m gathered counts (device, row s = rank s);
+ *     peer_keys / peer_vals = host arrays of G device pointers, the output
+ *     shard of every rank (peer_vals NULL: keys only); writes this rank's
+ *     elements into the owners' shards and, if global_bucket_offsets is not
+ *     NULL, the m+1 global bucket starts (uint64, device).
+ * ws: ms_shard_workspace_size(n_local, m, G, with_values) bytes.  Errors as
+ * for ms_multisplit_*, and MS_ERR_UNSUPPORTED for m > 32 on a device whose
+ * lane-order probe has not passed. */
+size_t ms_shard_workspace_size(uint64_t n_local, uint32_t m, uint32_t G, int with_values);
+ms_status ms_shard_prescan(const uint32_t *keys_in, uint64_t n_local, const ms_bucket_fn *fn,
+                           int with_values, uint32_t G, uint32_t *counts, void *ws, size_t ws_bytes,
+                           void *stream);
+ms_status ms_shard_scatter(const uint32_t *keys_in, const uint32_t *vals_in, uint64_t n_local,
+                           const ms_bucket_fn *fn, const uint32_t *C, uint32_t G, uint32_t rank,
+                           uint32_t *const *peer_keys, uint32_t *const *peer_vals,
+                           uint64_t *global_bucket_offsets, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
  * Instrumentation (host only, thread-local, zero cost when unset).

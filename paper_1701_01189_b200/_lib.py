@@ -69,6 +69,16 @@ SIGNATURES = [
     ("ms_shard_merge_pairs", _I, [_P, _P, _U64, _FN, _P, _P, _U32, _P, _P, _P]),
     ("ms_histogram_even", _I, [_P, _U64, _U32, ctypes.c_float, ctypes.c_float, _P, _P]),
     ("ms_histogram_range", _I, [_P, _U64, _U32, _P, _P, _P]),
+    ("ms_comm_unique_id", _I, [_P]),
+    ("ms_comm_init", _I, [ctypes.POINTER(ctypes.c_void_p), _I, _I, _P, _I]),
+    ("ms_comm_destroy", _I, [_P]),
+    ("ms_comm_register_output", _I, [_P, _P, _P, _U64]),
+    ("ms_sharded_workspace_size", _SZ, [_P, _U64, _U32, _I]),
+    ("ms_multisplit_keys_sharded", _I, [_P, _P, _P, _U64, _FN, _P, _P, _SZ, _P]),
+    ("ms_multisplit_pairs_sharded", _I, [_P, _P, _P, _P, _P, _U64, _FN, _P, _P, _SZ, _P]),
+    ("ms_shard_workspace_size", _SZ, [_U64, _U32, _U32, _I]),
+    ("ms_shard_prescan", _I, [_P, _U64, _FN, _I, _U32, _P, _P, _SZ, _P]),
+    ("ms_shard_scatter", _I, [_P, _P, _U64, _FN, _P, _U32, _U32, _P, _P, _P, _P, _SZ, _P]),
     ("ms_set_stage_events", None, [_P]),
     ("ms_launch_count", _U64, []),
 ]

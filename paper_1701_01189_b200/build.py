@@ -12,12 +12,24 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build", "ms")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include() -> str:
+    """NCCL headers: the venv's copy (the library PyTorch loads), else the system's."""
+    try:
+        import nvidia.nccl
+        for p in nvidia.nccl.__path__:
+            if os.path.exists(os.path.join(p, "include", "nccl.h")):
+                return os.path.join(p, "include")
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include"), "-I", _nccl_include()]
 
 SOURCES = ["ms_capi.cu", "ms_inst_identity.cu", "ms_inst_delta.cu", "ms_inst_radix.cu",
            "ms_inst_deltashift.cu", "ms_inst_topbits.cu"]
-HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_meta.cuh", "ms_dispatch.cuh", "ms_scan.cuh", "ms_hist.cuh"]
+HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_meta.cuh", "ms_wide.cuh", "ms_nccl.cuh", "ms_dispatch.cuh", "ms_scan.cuh", "ms_hist.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -50,7 +62,7 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     if _newer(out, objs):
         tmp = out + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
         os.replace(tmp, out)
     return out
 

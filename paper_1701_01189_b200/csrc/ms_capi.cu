@@ -2,6 +2,7 @@
 // argument validation, workspace carving, strategy dispatch and the LSD
 // radix-sort pass driver.  All launches are stream-ordered; nothing here
 // synchronizes except ms_device_status.
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <cmath>
@@ -13,6 +14,9 @@
 #include "ms_dispatch.cuh"
 #include "ms_hist.cuh"
 #include "ms_scan.cuh"
+#include "ms_nccl.cuh"
+
+#include <cuda.h>
 
 using namespace ms;
 
@@ -114,17 +118,21 @@ uint32_t ctas_per_sm(uint32_t m, bool pairs) {
 // Workspace: [hdr 256 B][base 1280 B][R or H: L*m words][KG status: nchunks*m u64]
 // (the level-0 histogram R needs G <= L rows; the three-launch mode needs L rows of H).
 struct Layout {
-  size_t base, H, status, meta, total;
+  size_t base, H, status, meta, wmeta, total;
   uint32_t T, L, nchunks, C, MS;
+  uint32_t LW, NB;  // m > 32: tiles and buckets per lane of the wide pipeline (ms_wide.cuh)
 };
+constexpr uint32_t kMaxRanges = 4096;  // level-0 ranges (CTAs) of the persistent kernels
 
 
-Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
+// ranges: always lay out the level-0 range pipeline (the sharded path has no
+// single-CTA shortcut)
+Layout layout_for(uint64_t n, uint32_t m, bool pairs, bool ranges = false) {
   Layout lo{};
   lo.T = tile_elems(m, pairs);
   lo.base = kHdrBytes;
   lo.H = kHdrBytes + kBaseBytes;
-  if (n <= lo.T) {  // single-CTA path: header only
+  if (n == 0 || (n <= lo.T && !ranges)) {  // single-CTA path: header only
     lo.status = lo.total = lo.H;
     lo.L = n ? 1 : 0;
     return lo;
@@ -132,12 +140,21 @@ Layout layout_for(uint64_t n, uint32_t m, bool pairs) {
   lo.L = (uint32_t)((n + lo.T - 1) / lo.T);
   lo.C = scan_chunk_tiles(m);
   lo.nchunks = (lo.L + lo.C - 1) / lo.C;
-  lo.status = lo.H + align_up((size_t)lo.L * m * 8u);  // H (or R and its prefixes P)
+  size_t hwords = (size_t)lo.L * m * 2u;  // H (or R and its prefixes P)
+  if (m > 32) {
+    lo.NB = wide_nb(m);
+    lo.LW = (uint32_t)((n + wide_tile(pairs) - 1) / wide_tile(pairs));
+    const size_t rw = 2u * (size_t)std::min(lo.LW, kMaxRanges) * 32u * lo.NB;
+    hwords = std::max(hwords, rw);
+  }
+  lo.status = lo.H + align_up(hwords * 4u);
   lo.total = lo.status + align_up((size_t)lo.nchunks * m * 8u);
-  lo.meta = lo.total;
+  lo.meta = lo.wmeta = lo.total;
   if (m <= 32) {  // tile meta records (ms_meta.cuh)
     lo.MS = meta_stride(meta_ms(m), kWarps);
     lo.total = lo.meta + align_up((size_t)lo.L * lo.MS * 4u);
+  } else {  // wide records (ms_wide.cuh)
+    lo.total = lo.wmeta + align_up((size_t)lo.LW * wide_rec_words(pairs, lo.NB) * 4u);
   }
   return lo;
 }
@@ -268,6 +285,28 @@ cudaError_t fused_meta(const Plan &pl, bool pairs, const KfArgs &a, uint32_t gri
   }
 }
 
+cudaError_t tile_meta_wide(const Plan &pl, bool pairs, const uint32_t *keys, uint32_t n, uint32_t LM,
+                           uint32_t per, uint32_t grid, uint32_t *meta, uint32_t nkf, uint32_t *R,
+                           uint32_t *hdr, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
+    case kDelta: return Launch<kDelta>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
+    case kRadix: return Launch<kRadix>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
+    case kTopBits: return Launch<kTopBits>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
+    default: return Launch<kDeltaShift>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
+  }
+}
+
+cudaError_t fused_meta_wide(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
+  switch (pl.kind) {
+    case kIdentity: return Launch<kIdentity>::fused_meta_wide(pairs, a, pl.bp, grid, s);
+    case kDelta: return Launch<kDelta>::fused_meta_wide(pairs, a, pl.bp, grid, s);
+    case kRadix: return Launch<kRadix>::fused_meta_wide(pairs, a, pl.bp, grid, s);
+    case kTopBits: return Launch<kTopBits>::fused_meta_wide(pairs, a, pl.bp, grid, s);
+    default: return Launch<kDeltaShift>::fused_meta_wide(pairs, a, pl.bp, grid, s);
+  }
+}
+
 cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
   switch (pl.kind) {
     case kIdentity: return Launch<kIdentity>::fused(pairs, a, pl.bp, grid, s);
@@ -276,6 +315,81 @@ cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cu
     case kTopBits: return Launch<kTopBits>::fused(pairs, a, pl.bp, grid, s);
     default: return Launch<kDeltaShift>::fused(pairs, a, pl.bp, grid, s);
   }
+}
+
+// Level-0 pipelines with prescan records: m <= 32 KM -> kf_meta (ms_meta.cuh),
+// 32 < m <= 256 KMW -> KR -> kf_meta_wide (ms_wide.cuh; increments only).
+struct L0 {
+  bool wide;
+  uint32_t G, K, mP, num_tiles;
+  uint32_t *R, *P, *Tot, *meta;
+};
+
+// the ranges and buffers of a call (pure host arithmetic: the sharded scatter
+// recomputes what its prescan used)
+L0 l0_setup(uint32_t m, bool pairs, const Layout &lo, char *w) {
+  L0 st{};
+  uint32_t *H = (uint32_t *)(w + lo.H);
+  st.Tot = (uint32_t *)(w + lo.base);
+  st.wide = m > 32;
+  if (!st.wide) {
+    const uint32_t target = std::min((uint32_t)sm_count() * ctas_per_sm(m, pairs), kMaxRanges);
+    st.K = (lo.L + target - 1) / target;
+    st.G = (lo.L + st.K - 1) / st.K;
+    st.mP = m;
+    st.num_tiles = lo.L;
+    st.R = H;
+    st.P = H + (size_t)st.G * m;
+    st.meta = (uint32_t *)(w + lo.meta);
+    return st;
+  }
+  // K even for pairs so that a KM tile (8192 keys = two pair tiles) never
+  // straddles two ranges
+  st.mP = 32u * lo.NB;
+  const uint32_t target = std::min((uint32_t)sm_count() * 2u, kMaxRanges);
+  st.K = (lo.LW + target - 1) / target;
+  if (pairs && (st.K & 1u)) ++st.K;
+  st.G = (lo.LW + st.K - 1) / st.K;
+  st.num_tiles = lo.LW;
+  st.R = H;
+  st.P = H + (size_t)st.G * st.mP;
+  st.meta = (uint32_t *)(w + lo.wmeta);
+  return st;
+}
+
+// with_totals: also the bucket totals Tot (m <= 32: an extra KR launch; the
+// wide pipeline always has them)
+cudaError_t l0_prescan(const Plan &pl, bool pairs, const uint32_t *keys, uint32_t n, const Layout &lo,
+                       char *w, bool with_totals, L0 &st, cudaStream_t s) {
+  const uint32_t m = pl.bp.m;
+  uint32_t *hdr = (uint32_t *)w;
+  st = l0_setup(m, pairs, lo, w);
+  if (!st.wide) {
+    cudaError_t e = counted(tile_meta(pl, pairs, keys, n, lo.L, st.K, st.G, st.meta, st.R, hdr, s));
+    if (e == cudaSuccess && with_totals)
+      e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.G, m, s));
+    return e;
+  }
+  const uint32_t per_km = pairs ? st.K / 2u : st.K;
+  const uint32_t LM = (uint32_t)((n + kWideKmTile - 1) / kWideKmTile);
+  cudaError_t e = counted(tile_meta_wide(pl, pairs, keys, n, LM, per_km, st.G, st.meta, lo.LW, st.R, hdr, s));
+  if (e == cudaSuccess) e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.G, st.mP, s));
+  return e;
+}
+
+cudaError_t l0_postscan(const Plan &pl, bool pairs, KfArgs &a, const L0 &st, cudaStream_t s) {
+  a.mode = kModeRange;
+  a.meta = st.meta;
+  a.num_tiles = st.num_tiles;
+  a.tiles_per_cta = st.K;
+  a.num_ranges = st.G;
+  if (!st.wide) {
+    a.R = st.R;  // kf_meta reduces the range histograms itself
+    return counted(fused_meta(pl, pairs, a, st.G, s));
+  }
+  a.R = st.P;
+  a.Tot = st.Tot;
+  return counted(fused_meta_wide(pl, pairs, a, st.G, s));
 }
 
 ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
@@ -326,9 +440,9 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   // Eq.4 term 1 by lane-ordered increments (reading R23) only on a device whose
   // probe passed and unless deterministic peer masks are requested; measured
   // (profiles/r01/s2_summary.md): increments win for keys and for m <= 32
-  a.rank_inc = m > 2 && (!pairs || m <= 32) &&
-               g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
-               ms::lane_ordered_inc(false) == 1;
+  const bool inc_ok = m > 2 && g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
+                      ms::lane_ordered_inc(false) == 1;
+  a.rank_inc = inc_ok && (!pairs || m <= 32);
 
   if (n <= lo.T) {  // one subproblem: a single launch
     a.mode = kModeSingle;
@@ -369,36 +483,29 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   }
 
   // level-0 localization (Eq.3 with L_0 = G): G ranges of K consecutive tiles,
-  // one CTA each.  KU: range histograms R (m x G); KR: column scan P of R and
-  // the bucket totals; KF: bucket bases from the totals, then per range, tiles
-  // in order with running per-bucket offsets.  KR and KF are programmatic
-  // dependent launches.
-  const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
-  const uint32_t K = (lo.L + target - 1) / target;
-  const uint32_t G = (lo.L + K - 1) / K;
-  const bool meta_mode = m <= 32;
-  uint32_t *meta = (uint32_t *)(w + lo.meta);
-  stage_event(0, s);
-  if (meta_mode) {
-    if (counted(tile_meta(pl, pairs, keys_in, (uint32_t)n, lo.L, K, G, meta, H, hdr, s)) !=
-        cudaSuccess)
+  // one CTA each, tiles in order with running per-bucket offsets
+  if (m <= 32 || inc_ok) {  // prescan records + rank/reorder postscan (ms_meta / ms_wide)
+    L0 st{};
+    stage_event(0, s);
+    if (l0_prescan(pl, pairs, keys_in, (uint32_t)n, lo, w, false, st, s) != cudaSuccess)
       return MS_ERR_CUDA;
-  } else if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess) {
-    return MS_ERR_CUDA;
-  }
-  stage_event(1, s);
-  uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
-  if (meta_mode) {  // KF reduces the range histograms itself (no KR)
+    stage_event(1, s);
     stage_event(2, s);
-    a.mode = kModeRange;
-    a.R = H;
-    a.tiles_per_cta = K;
-    a.num_ranges = G;
-    a.meta = meta;
-    const cudaError_t e = counted(fused_meta(pl, pairs, a, G, s));
+    const cudaError_t e = l0_postscan(pl, pairs, a, st, s);
     stage_event(3, s);
     return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
   }
+  // m > 32 with deterministic ranks: KU range histograms R (m x G) -> KR column
+  // scan P of R and the bucket totals -> KF (kf_fused) counts, scans and ranks
+  // each tile itself.  KR and KF are programmatic dependent launches.
+  const uint32_t target = (uint32_t)sm_count() * ctas_per_sm(m, pairs);
+  const uint32_t K = (lo.L + target - 1) / target;
+  const uint32_t G = (lo.L + K - 1) / K;
+  stage_event(0, s);
+  if (counted(range_hist(pl, keys_in, (uint32_t)n, K * lo.T, G, H, hdr, s)) != cudaSuccess)
+    return MS_ERR_CUDA;
+  stage_event(1, s);
+  uint32_t *P = H + (size_t)G * m;  // prefixes (the layout holds 2 L m words)
   if (counted(launch_level0_scan(H, P, base, G, m, s)) != cudaSuccess) return MS_ERR_CUDA;
   stage_event(2, s);
   a.mode = kModeRange;
@@ -792,6 +899,467 @@ ms_status ms_shard_merge_pairs(const uint32_t *keys_recv, const uint32_t *vals_r
                                uint32_t G, uint32_t *keys_out, uint32_t *vals_out, void *stream) {
   return shard_merge(keys_recv, vals_recv, n_recv, fn, recv_starts, merge_offsets, G, keys_out,
                      vals_out, stream, true);
+}
+
+// ---------------------------------------------------------------- sharded (Eq.3, GPUs as level 0)
+}  // extern "C"
+
+// KPP: the rank's global bucket bases (Eq.3 terms 1-2 with L_0 = G ranks)
+//   gb[b] = sum_{b'<b} sum_s C[s][b'] + sum_{s<r} C[s][b],
+// the output shard starts pstart[s] = sum_{s'<s} n_s' (n_s = sum_b C[s][b],
+// pstart[G] = n_total) and the global bucket offsets gofs[0..m].  One CTA.
+static __global__ void __launch_bounds__(256)
+    k_shard_plan(const uint32_t *__restrict__ C, uint32_t G, uint32_t r, uint32_t m,
+                 uint32_t *__restrict__ gb, uint32_t *__restrict__ pstart,
+                 unsigned long long *__restrict__ gofs) {
+  __shared__ uint32_t s_w[8];
+  __shared__ uint32_t s_n[kMaxPeers];
+  const uint32_t b = threadIdx.x, lane = b & 31u, warp = b >> 5;
+  uint32_t col = 0, below = 0;
+  for (uint32_t sr = 0; sr < G; ++sr) {
+    const uint32_t c = b < m ? C[(size_t)sr * m + b] : 0u;
+    col += c;
+    below += sr < r ? c : 0u;
+    uint32_t t = c;  // n_s: block reduction of row s
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+    if (lane == 0) s_w[warp] = t;
+    __syncthreads();
+    if (b == 0) {
+      uint32_t x = 0;
+      for (int w = 0; w < 8; ++w) x += s_w[w];
+      s_n[sr] = x;
+    }
+    __syncthreads();
+  }
+  uint32_t incl = col;  // exclusive scan of the column sums over the buckets
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0;
+  for (uint32_t w = 0; w < warp; ++w) wpre += s_w[w];
+  const uint32_t A = wpre + incl - col;
+  if (b < m) {
+    gb[b] = A + below;
+    if (gofs) {
+      gofs[b] = A;
+      if (b == m - 1) gofs[m] = A + col;
+    }
+  }
+  if (b == 0) {
+    uint32_t x = 0;
+    for (uint32_t sr = 0; sr < G; ++sr) {
+      pstart[sr] = x;
+      x += s_n[sr];
+    }
+    pstart[G] = x;
+  }
+}
+
+struct ms_comm {
+  int nranks = 0, rank = 0, device = 0;
+  ncclComm_t nccl = nullptr;
+  uint32_t *d_scratch = nullptr;  // handle exchange + barrier word
+  // registered output windows (KP)
+  uint32_t *win_k = nullptr, *win_v = nullptr;
+  uint64_t win_n = 0;
+  uint32_t *peer_k[kMaxPeers] = {}, *peer_v[kMaxPeers] = {};
+  void *opened[2 * kMaxPeers] = {};
+  int nopened = 0;
+  // NCCL path: pinned host buffers of the plan, and the event of their last H2D
+  uint32_t *h_offs = nullptr;
+  unsigned char *h_plan = nullptr;
+  cudaEvent_t plan_done = nullptr;
+};
+
+namespace {
+
+constexpr size_t kShardScratch = 4096;
+constexpr size_t kPlanBytes = (size_t)kMaxPeers * 256 * 4 + (kMaxPeers + 1) * 4 + 257 * 8 + 256;
+
+// the KP state after the level-0 layout of the local shard: [C_all G x m][gb m][pstart G+1]
+struct ShardLayout {
+  Layout lo;
+  size_t C, gb, pstart, total;
+};
+ShardLayout shard_layout(uint64_t n, uint32_t m, uint32_t G, bool pairs) {
+  ShardLayout sl{};
+  sl.lo = layout_for(n, m, pairs, true);
+  sl.C = align_up(sl.lo.total);
+  sl.gb = sl.C + align_up((size_t)G * m * 4u);
+  sl.pstart = sl.gb + align_up((size_t)m * 4u);
+  sl.total = sl.pstart + align_up((size_t)(G + 1) * 4u);
+  return sl;
+}
+
+bool kp_supported(uint32_t m) {
+  return m <= 32 || (g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
+                     ms::lane_ordered_inc(false) == 1);
+}
+
+ms_status shard_check(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn, void *ws) {
+  ms_status st = validate_fn(fn);
+  if (st != MS_SUCCESS) return st;
+  if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
+  if (!ws || ((uintptr_t)ws & (kAlign - 1))) return MS_ERR_INVALID_VALUE;
+  if (n > 0 && !keys_in) return MS_ERR_INVALID_VALUE;
+  return MS_SUCCESS;
+}
+
+ms_status shard_prescan_impl(const uint32_t *keys_in, uint64_t n, const ms_bucket_fn *fn, bool pairs,
+                             uint32_t G, uint32_t *counts, void *ws, size_t ws_bytes,
+                             cudaStream_t s) {
+  ms_status st = shard_check(keys_in, n, fn, ws);
+  if (st != MS_SUCCESS) return st;
+  const uint32_t m = fn->num_buckets;
+  if (!kp_supported(m)) return MS_ERR_UNSUPPORTED;
+  const ShardLayout sl = shard_layout(n, m, G, pairs);
+  if (ws_bytes < sl.total) return MS_ERR_WORKSPACE;
+  char *w = (char *)ws;
+  if (n == 0) {
+    if (cudaMemsetAsync(w, 0, 8, s) != cudaSuccess) return MS_ERR_CUDA;
+    if (counts && cudaMemsetAsync(counts, 0, (size_t)m * 4u, s) != cudaSuccess) return MS_ERR_CUDA;
+    return MS_SUCCESS;
+  }
+  const Plan pl = make_plan(fn);
+  L0 l0{};
+  if (l0_prescan(pl, pairs, keys_in, (uint32_t)n, sl.lo, w, true, l0, s) != cudaSuccess)
+    return MS_ERR_CUDA;
+  if (counts && cudaMemcpyAsync(counts, l0.Tot, (size_t)m * 4u, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return MS_ERR_CUDA;
+  return MS_SUCCESS;
+}
+
+ms_status shard_scatter_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint64_t n,
+                             const ms_bucket_fn *fn, const uint32_t *C, uint32_t G, uint32_t r,
+                             uint32_t *const *peer_k, uint32_t *const *peer_v,
+                             uint64_t *gofs, void *ws, size_t ws_bytes, cudaStream_t s,
+                             bool pairs) {
+  ms_status st = shard_check(keys_in, n, fn, ws);
+  if (st != MS_SUCCESS) return st;
+  const uint32_t m = fn->num_buckets;
+  if (!kp_supported(m)) return MS_ERR_UNSUPPORTED;
+  if (G == 0 || G > kMaxPeers || r >= G || !C || !peer_k) return MS_ERR_INVALID_VALUE;
+  if (pairs && (!peer_v || (n > 0 && !vals_in))) return MS_ERR_INVALID_VALUE;
+  for (uint32_t d = 0; d < G; ++d)
+    if (!peer_k[d] || (pairs && !peer_v[d])) return MS_ERR_INVALID_VALUE;
+  const ShardLayout sl = shard_layout(n, m, G, pairs);
+  if (ws_bytes < sl.total) return MS_ERR_WORKSPACE;
+  char *w = (char *)ws;
+  uint32_t *gb = (uint32_t *)(w + sl.gb), *pstart = (uint32_t *)(w + sl.pstart);
+  k_shard_plan<<<1, 256, 0, s>>>(C, G, r, m, gb, pstart, (unsigned long long *)gofs);
+  if (counted(cudaGetLastError()) != cudaSuccess) return MS_ERR_CUDA;
+  if (n == 0) return MS_SUCCESS;
+  const Plan pl = make_plan(fn);
+  L0 l0 = l0_setup(m, pairs, sl.lo, w);
+  KfArgs a{};
+  a.keys_in = keys_in;
+  a.vals_in = pairs ? vals_in : nullptr;
+  a.keys_out = peer_k[r];
+  a.vals_out = pairs ? peer_v[r] : nullptr;
+  a.n = (uint32_t)n;
+  a.hdr = (uint32_t *)w;
+  a.bucket_offsets = nullptr;
+  a.use_tma = (((uintptr_t)keys_in & 15u) == 0) && (!pairs || (((uintptr_t)vals_in & 15u) == 0));
+  a.store_runs = 0;  // per-element stores into the owners' windows
+  a.rank_inc = m > 2 && g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
+               ms::lane_ordered_inc(false) == 1;
+  a.gbase_ovr = gb;
+  a.peer_start = pstart;
+  a.npeers = G;
+  for (uint32_t d = 0; d < G; ++d) {
+    a.peer_k[d] = peer_k[d];
+    a.peer_v[d] = pairs ? peer_v[d] : nullptr;
+  }
+  return l0_postscan(pl, pairs, a, l0, s) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+}
+
+// NCCL path workspace: [local multisplit ws][stage k, v][recv k, v][offs G x (m+1)][merge G x m][starts G+1]
+struct NcclLayout {
+  size_t ms, stage_k, stage_v, recv_k, recv_v, offs, merge, starts, total;
+};
+NcclLayout nccl_layout(uint64_t n, uint32_t m, uint32_t G, bool pairs) {
+  NcclLayout L{};
+  L.ms = 0;
+  const size_t nb = align_up(n * 4u);
+  L.stage_k = align_up(layout_for(n, m, pairs).total);
+  L.stage_v = L.stage_k + nb;
+  L.recv_k = L.stage_v + (pairs ? nb : 0);
+  L.recv_v = L.recv_k + nb;
+  L.offs = L.recv_v + (pairs ? nb : 0);
+  L.merge = L.offs + align_up((size_t)G * (m + 1) * 4u);
+  L.starts = L.merge + align_up((size_t)G * m * 4u);
+  L.total = L.starts + align_up((size_t)(G + 1) * 4u);
+  return L;
+}
+
+ms_status nccl_status(ncclResult_t r) { return r == ncclSuccess ? MS_SUCCESS : MS_ERR_NCCL; }
+
+ms_status sharded_impl(ms_comm *c, const uint32_t *keys_in, const uint32_t *vals_in,
+                       uint32_t *keys_out, uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
+                       uint64_t *gofs, void *ws, size_t ws_bytes, void *stream, bool pairs) {
+  if (!c) return MS_ERR_INVALID_VALUE;
+  ms_status st = shard_check(keys_in, n, fn, ws);
+  if (st != MS_SUCCESS) return st;
+  if (n > 0 && (!keys_out || (pairs && (!vals_in || !vals_out)))) return MS_ERR_INVALID_VALUE;
+  if (ws_bytes < ms_sharded_workspace_size(c, n, fn->num_buckets, pairs)) return MS_ERR_WORKSPACE;
+  const NcclApi &nc = nccl();
+  if (!nc.ok) return MS_ERR_NCCL;
+  const uint32_t m = fn->num_buckets, G = (uint32_t)c->nranks, r = (uint32_t)c->rank;
+  cudaStream_t s = (cudaStream_t)stream;
+  char *w = (char *)ws;
+  const bool kp = c->win_k == keys_out && c->win_n == n && (!pairs || c->win_v == vals_out) &&
+                  kp_supported(m);
+  if (kp) {
+    // KP: prescan -> all-gather of the G x m counts -> plan + fused scatter into
+    // the owners' windows -> all-reduce of one word as the completion barrier
+    const ShardLayout sl = shard_layout(n, m, G, pairs);
+    uint32_t *C = (uint32_t *)(w + sl.C);
+    st = shard_prescan_impl(keys_in, n, fn, pairs, G, C + (size_t)r * m, ws, ws_bytes, s);
+    if (st != MS_SUCCESS) return st;
+    if (nc.AllGather(C + (size_t)r * m, C, m, ncclUint32, c->nccl, s) != ncclSuccess) return MS_ERR_NCCL;
+    st = shard_scatter_impl(keys_in, vals_in, n, fn, C, G, r, c->peer_k, c->peer_v, gofs, ws, ws_bytes,
+                            s, pairs);
+    if (st != MS_SUCCESS) return st;
+    return nccl_status(nc.AllReduce(c->d_scratch, c->d_scratch, 1, ncclUint32, ncclSum, c->nccl, s));
+  }
+  // NCCL path: local multisplit -> all-gather of the bucket offsets -> host
+  // plan (one D2H + stream sync) -> send / receive of contiguous ranges -> KX merge
+  const NcclLayout L = nccl_layout(n, m, G, pairs);
+  uint32_t *sk = (uint32_t *)(w + L.stage_k), *sv = (uint32_t *)(w + L.stage_v);
+  uint32_t *rk = (uint32_t *)(w + L.recv_k), *rv = (uint32_t *)(w + L.recv_v);
+  uint32_t *offs = (uint32_t *)(w + L.offs), *merge = (uint32_t *)(w + L.merge);
+  uint32_t *starts = (uint32_t *)(w + L.starts);
+  st = multisplit_impl(keys_in, pairs ? vals_in : nullptr, sk, pairs ? sv : nullptr, n, fn,
+                       offs + (size_t)r * (m + 1), ws, L.stage_k, stream, pairs);
+  if (st != MS_SUCCESS) return st;
+  if (nc.AllGather(offs + (size_t)r * (m + 1), offs, m + 1, ncclUint32, c->nccl, s) != ncclSuccess)
+    return MS_ERR_NCCL;
+  if (c->plan_done && cudaEventSynchronize(c->plan_done) != cudaSuccess) return MS_ERR_CUDA;
+  if (cudaMemcpyAsync(c->h_offs, offs, (size_t)G * (m + 1) * 4u, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return MS_ERR_CUDA;
+  std::vector<uint64_t> Ch((size_t)G * m), sc(G), sd(G), rc(G), rd(G), go(m + 1);
+  for (uint32_t q = 0; q < G; ++q)
+    for (uint32_t j = 0; j < m; ++j)
+      Ch[(size_t)q * m + j] = c->h_offs[(size_t)q * (m + 1) + j + 1] - c->h_offs[(size_t)q * (m + 1) + j];
+  uint32_t *h_merge = (uint32_t *)c->h_plan;
+  uint32_t *h_starts = h_merge + (size_t)G * m;
+  uint64_t *h_gofs = (uint64_t *)(c->h_plan + align_up(((size_t)G * m + G + 1) * 4u));
+  st = ms_shard_plan(Ch.data(), G, m, r, sc.data(), sd.data(), rc.data(), rd.data(), h_merge, h_gofs);
+  if (st != MS_SUCCESS) return st;
+  uint64_t nrecv = 0;
+  for (uint32_t q = 0; q < G; ++q) {
+    h_starts[q] = (uint32_t)rd[q];
+    nrecv += rc[q];
+  }
+  h_starts[G] = (uint32_t)nrecv;
+  if (cudaMemcpyAsync(merge, h_merge, ((size_t)G * m + G + 1) * 4u, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return MS_ERR_CUDA;
+  if (gofs && cudaMemcpyAsync(gofs, h_gofs, (m + 1) * 8u, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return MS_ERR_CUDA;
+  if (cudaEventRecord(c->plan_done, s) != cudaSuccess) return MS_ERR_CUDA;
+  if (nc.GroupStart() != ncclSuccess) return MS_ERR_NCCL;
+  for (uint32_t d = 0; d < G; ++d) {
+    if (d == r) continue;
+    if (sc[d]) {
+      nc.Send(sk + sd[d], sc[d], ncclUint32, (int)d, c->nccl, s);
+      if (pairs) nc.Send(sv + sd[d], sc[d], ncclUint32, (int)d, c->nccl, s);
+    }
+    if (rc[d]) {
+      nc.Recv(rk + rd[d], rc[d], ncclUint32, (int)d, c->nccl, s);
+      if (pairs) nc.Recv(rv + rd[d], rc[d], ncclUint32, (int)d, c->nccl, s);
+    }
+  }
+  if (nc.GroupEnd() != ncclSuccess) return MS_ERR_NCCL;
+  if (sc[r]) {  // this rank's own part: a device copy
+    if (cudaMemcpyAsync(rk + rd[r], sk + sd[r], sc[r] * 4u, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        (pairs && cudaMemcpyAsync(rv + rd[r], sv + sd[r], sc[r] * 4u, cudaMemcpyDeviceToDevice, s) != cudaSuccess))
+      return MS_ERR_CUDA;
+  }
+  return pairs ? ms_shard_merge_pairs(rk, rv, nrecv, fn, starts, merge, G, keys_out, vals_out, stream)
+               : ms_shard_merge_keys(rk, nrecv, fn, starts, merge, G, keys_out, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ms_shard_workspace_size(uint64_t n_local, uint32_t m, uint32_t G, int with_values) {
+  if (m < 1) m = 1;
+  if (m > 256) m = 256;
+  if (G < 1) G = 1;
+  return shard_layout(n_local, m, G, with_values != 0).total;
+}
+
+ms_status ms_shard_prescan(const uint32_t *keys_in, uint64_t n_local, const ms_bucket_fn *fn,
+                           int with_values, uint32_t G, uint32_t *counts, void *ws, size_t ws_bytes,
+                           void *stream) {
+  return shard_prescan_impl(keys_in, n_local, fn, with_values != 0, G, counts, ws, ws_bytes,
+                            (cudaStream_t)stream);
+}
+
+ms_status ms_shard_scatter(const uint32_t *keys_in, const uint32_t *vals_in, uint64_t n_local,
+                           const ms_bucket_fn *fn, const uint32_t *C, uint32_t G, uint32_t rank,
+                           uint32_t *const *peer_keys, uint32_t *const *peer_vals,
+                           uint64_t *global_bucket_offsets, void *ws, size_t ws_bytes, void *stream) {
+  return shard_scatter_impl(keys_in, vals_in, n_local, fn, C, G, rank, peer_keys, peer_vals,
+                            global_bucket_offsets, ws, ws_bytes, (cudaStream_t)stream,
+                            peer_vals != nullptr);
+}
+
+ms_status ms_comm_unique_id(void *out128) {
+  if (!out128) return MS_ERR_INVALID_VALUE;
+  const NcclApi &nc = nccl();
+  if (!nc.ok) return MS_ERR_NCCL;
+  ncclUniqueId id;
+  if (nc.GetUniqueId(&id) != ncclSuccess) return MS_ERR_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return MS_SUCCESS;
+}
+
+ms_status ms_comm_init(ms_comm **out, int nranks, int rank, const void *id128, int cuda_device) {
+  if (!out || !id128 || nranks < 1 || nranks > (int)kMaxPeers || rank < 0 || rank >= nranks)
+    return MS_ERR_INVALID_VALUE;
+  const NcclApi &nc = nccl();
+  if (!nc.ok) return MS_ERR_NCCL;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return MS_ERR_CUDA;
+  ms_comm *c = new ms_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = cuda_device;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ms_status st = MS_SUCCESS;
+  if (nc.CommInitRank(&c->nccl, nranks, id, rank) != ncclSuccess) st = MS_ERR_NCCL;
+  if (st == MS_SUCCESS && (cudaMalloc((void **)&c->d_scratch, kShardScratch) != cudaSuccess ||
+                           cudaMemset(c->d_scratch, 0, kShardScratch) != cudaSuccess ||
+                           cudaMallocHost((void **)&c->h_offs, (size_t)kMaxPeers * 257 * 4) != cudaSuccess ||
+                           cudaMallocHost((void **)&c->h_plan, kPlanBytes) != cudaSuccess ||
+                           cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming) != cudaSuccess))
+    st = MS_ERR_CUDA;
+  if (st != MS_SUCCESS) {
+    ms_comm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return MS_SUCCESS;
+}
+
+ms_status ms_comm_destroy(ms_comm *c) {
+  if (!c) return MS_ERR_INVALID_VALUE;
+  for (int i = 0; i < c->nopened; ++i) cudaIpcCloseMemHandle(c->opened[i]);
+  if (c->nccl) nccl().CommDestroy(c->nccl);
+  if (c->d_scratch) cudaFree(c->d_scratch);
+  if (c->h_offs) cudaFreeHost(c->h_offs);
+  if (c->h_plan) cudaFreeHost(c->h_plan);
+  if (c->plan_done) cudaEventDestroy(c->plan_done);
+  delete c;
+  return MS_SUCCESS;
+}
+
+ms_status ms_comm_register_output(ms_comm *c, uint32_t *keys_out, uint32_t *vals_out,
+                                  uint64_t n_local) {
+  if (!c || !keys_out) return MS_ERR_INVALID_VALUE;
+  const NcclApi &nc = nccl();
+  if (!nc.ok) return MS_ERR_NCCL;
+  for (int i = 0; i < c->nopened; ++i) cudaIpcCloseMemHandle(c->opened[i]);
+  c->nopened = 0;
+  c->win_k = c->win_v = nullptr;
+  // per rank: {keys handle, keys offset, values handle, values offset, has values}
+  struct Rec {
+    cudaIpcMemHandle_t hk, hv;
+    unsigned long long ok, ov, has_v, pad;
+  };
+  static_assert(sizeof(Rec) % 16 == 0, "record size");
+  Rec mine{};
+  // the allocation that holds p (driver entry point: libms does not link libcuda)
+  using GetRange = CUresult (*)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static GetRange get_range = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range) return MS_ERR_CUDA;
+  auto handle = [](void *p, cudaIpcMemHandle_t *h, unsigned long long *off) {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+    *off = (unsigned long long)((CUdeviceptr)p - base);
+    return cudaIpcGetMemHandle(h, (void *)base) == cudaSuccess;
+  };
+  if (c->nranks > 1) {
+    if (!handle(keys_out, &mine.hk, &mine.ok)) return MS_ERR_CUDA;
+    if (vals_out && !handle(vals_out, &mine.hv, &mine.ov)) return MS_ERR_CUDA;
+  }
+  mine.has_v = vals_out ? 1u : 0u;
+  const size_t rb = sizeof(Rec);
+  if (rb * (size_t)c->nranks > kShardScratch) return MS_ERR_UNSUPPORTED;
+  unsigned char *d = (unsigned char *)c->d_scratch;
+  std::vector<Rec> all(c->nranks);
+  if (cudaMemcpy(d + rb * c->rank, &mine, rb, cudaMemcpyHostToDevice) != cudaSuccess) return MS_ERR_CUDA;
+  if (nc.AllGather(d + rb * c->rank, d, rb, ncclUint8, c->nccl, nullptr) != ncclSuccess) return MS_ERR_NCCL;
+  if (cudaMemcpy(all.data(), d, rb * c->nranks, cudaMemcpyDeviceToHost) != cudaSuccess) return MS_ERR_CUDA;
+  if (cudaMemset(c->d_scratch, 0, kShardScratch) != cudaSuccess) return MS_ERR_CUDA;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->peer_k[q] = keys_out;
+      c->peer_v[q] = vals_out;
+      continue;
+    }
+    void *pk = nullptr, *pv = nullptr;
+    if (cudaIpcOpenMemHandle(&pk, all[q].hk, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return MS_ERR_CUDA;
+    c->opened[c->nopened++] = pk;
+    c->peer_k[q] = (uint32_t *)((char *)pk + all[q].ok);
+    c->peer_v[q] = nullptr;
+    if (all[q].has_v) {
+      if (std::memcmp(&all[q].hv, &all[q].hk, sizeof(cudaIpcMemHandle_t)) == 0) {
+        pv = pk;  // values in the same allocation as the keys
+      } else {
+        if (cudaIpcOpenMemHandle(&pv, all[q].hv, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+          return MS_ERR_CUDA;
+        c->opened[c->nopened++] = pv;
+      }
+      c->peer_v[q] = (uint32_t *)((char *)pv + all[q].ov);
+    }
+  }
+  c->win_k = keys_out;
+  c->win_v = vals_out;
+  c->win_n = n_local;
+  return MS_SUCCESS;
+}
+
+size_t ms_sharded_workspace_size(const ms_comm *c, uint64_t n_local, uint32_t m, int with_values) {
+  if (m < 1) m = 1;
+  if (m > 256) m = 256;
+  const uint32_t G = c ? (uint32_t)c->nranks : 1u;
+  const size_t kp = shard_layout(n_local, m, G, with_values != 0).total;
+  const size_t nccl_path = nccl_layout(n_local, m, G, with_values != 0).total;
+  return kp > nccl_path ? kp : nccl_path;
+}
+
+ms_status ms_multisplit_keys_sharded(ms_comm *c, const uint32_t *keys_in, uint32_t *keys_out,
+                                     uint64_t n_local, const ms_bucket_fn *fn,
+                                     uint64_t *global_bucket_offsets, void *ws, size_t ws_bytes,
+                                     void *stream) {
+  return sharded_impl(c, keys_in, nullptr, keys_out, nullptr, n_local, fn, global_bucket_offsets, ws,
+                      ws_bytes, stream, false);
+}
+
+ms_status ms_multisplit_pairs_sharded(ms_comm *c, const uint32_t *keys_in, const uint32_t *vals_in,
+                                      uint32_t *keys_out, uint32_t *vals_out, uint64_t n_local,
+                                      const ms_bucket_fn *fn, uint64_t *global_bucket_offsets,
+                                      void *ws, size_t ws_bytes, void *stream) {
+  return sharded_impl(c, keys_in, vals_in, keys_out, vals_out, n_local, fn, global_bucket_offsets, ws,
+                      ws_bytes, stream, true);
 }
 
 void ms_set_stage_events(void *const *events) { g_stage_events = events; }

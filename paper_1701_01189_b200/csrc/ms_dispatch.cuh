@@ -6,7 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "ms_meta.cuh"
+#include "ms_wide.cuh"
 
 #include <atomic>
 
@@ -43,6 +43,13 @@ struct Launch {
                                uint32_t *meta, uint32_t *R, uint32_t *hdr, cudaStream_t s);
   static cudaError_t fused_meta(bool pairs, const KfArgs &a, const BucketParams &bp,
                                 uint32_t grid, cudaStream_t s);
+  // 32 < m <= 256 with warp offsets from the prescan (ms_wide.cuh)
+  static cudaError_t tile_meta_wide(bool pairs, const uint32_t *keys, uint32_t n, uint32_t num_tiles,
+                                    uint32_t tiles_per_cta, uint32_t grid, const BucketParams &bp,
+                                    uint32_t *meta, uint32_t num_kf_tiles, uint32_t *R, uint32_t *hdr,
+                                    cudaStream_t s);
+  static cudaError_t fused_meta_wide(bool pairs, const KfArgs &a, const BucketParams &bp,
+                                     uint32_t grid, cudaStream_t s);
   static cudaError_t merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
                            const BucketParams &bp, const uint32_t *starts, const uint32_t *offs,
                            uint32_t G, uint32_t *keys_out, uint32_t *vals_out, cudaStream_t s);
@@ -170,6 +177,61 @@ cudaError_t Launch<KIND>::fused_meta(bool pairs, const KfArgs &a, const BucketPa
                  : kfm_go<KIND, false, false, kRankInc>(a, bp, grid, s);
   return pairs ? kfm_go<KIND, true, false, kRankMasks>(a, bp, grid, s)
                : kfm_go<KIND, false, false, kRankMasks>(a, bp, grid, s);
+}
+
+template <int KIND, int NB, bool PAIRS>
+static cudaError_t kmw_go(const uint32_t *keys, uint32_t n, uint32_t num_tiles, uint32_t per,
+                          uint32_t grid, const BucketParams &bp, uint32_t *meta, uint32_t nkf,
+                          uint32_t *R, uint32_t *hdr, cudaStream_t s) {
+  auto kern = km_meta_wide<KIND, NB, PAIRS>;
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t e = set_max_smem(kern, kmw_smem_bytes(NB), done);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads + 32, kmw_smem_bytes(NB), s>>>(keys, n, num_tiles, per, bp, meta, nkf, R, hdr);
+  return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t Launch<KIND>::tile_meta_wide(bool pairs, const uint32_t *keys, uint32_t n,
+                                         uint32_t num_tiles, uint32_t per, uint32_t grid,
+                                         const BucketParams &bp, uint32_t *meta, uint32_t nkf,
+                                         uint32_t *R, uint32_t *hdr, cudaStream_t s) {
+  const uint32_t nb = wide_nb(bp.m);
+#define MS_KMW(NB_) \
+  return pairs ? kmw_go<KIND, NB_, true>(keys, n, num_tiles, per, grid, bp, meta, nkf, R, hdr, s) \
+               : kmw_go<KIND, NB_, false>(keys, n, num_tiles, per, grid, bp, meta, nkf, R, hdr, s)
+  if (nb == 2) { MS_KMW(2); }
+  if (nb == 4) { MS_KMW(4); }
+  MS_KMW(8);
+#undef MS_KMW
+}
+
+template <int KIND, bool PAIRS, int NB>
+static cudaError_t kfw_go(const KfArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
+  auto kern = kf_meta_wide<KIND, PAIRS, NB>;
+  static std::atomic<unsigned long long> done{0};
+  const cudaError_t e = set_max_smem(kern, kfw_smem_bytes(PAIRS, NB), done);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(wide_kw(PAIRS) * 32);
+  cfg.dynamicSmemBytes = kfw_smem_bytes(PAIRS, NB);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;  // right after our own KR
+  return cudaLaunchKernelEx(&cfg, kern, a, bp);
+}
+
+template <int KIND>
+cudaError_t Launch<KIND>::fused_meta_wide(bool pairs, const KfArgs &a, const BucketParams &bp,
+                                          uint32_t grid, cudaStream_t s) {
+  const uint32_t nb = wide_nb(bp.m);
+  if (nb == 2) return pairs ? kfw_go<KIND, true, 2>(a, bp, grid, s) : kfw_go<KIND, false, 2>(a, bp, grid, s);
+  if (nb == 4) return pairs ? kfw_go<KIND, true, 4>(a, bp, grid, s) : kfw_go<KIND, false, 4>(a, bp, grid, s);
+  return pairs ? kfw_go<KIND, true, 8>(a, bp, grid, s) : kfw_go<KIND, false, 8>(a, bp, grid, s);
 }
 
 template <int KIND>

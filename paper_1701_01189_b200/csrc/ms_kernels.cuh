@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(kThreads)
 // ============================================================================
 // KF: scan + postscan.
 // ============================================================================
+constexpr uint32_t kMaxPeers = 8;  // ranks of one node (sharded fused scatter)
+
 enum KfMode : int {
   kModeRange = 0,   // offsets from the range histograms R (two launches: KU, KF)
   kModeTileG = 1,   // offsets G[l][j] given per tile (three launches: KH, KG, KF)
@@ -243,7 +245,28 @@ struct KfArgs {
   int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
   int rank_inc;    // rank by lane-ordered shared-memory increments (reading R23, probed per device)
+  // sharded fused scatter (KP, Eq.3 with the GPUs as level 0): the bucket bases
+  // are the global A_b + B_{b,r} and every element goes to the output window of
+  // the rank that owns its global position (kf_meta / kf_meta_wide only)
+  const uint32_t *gbase_ovr;   // [m] global bucket bases of this rank, or null (local)
+  const uint32_t *peer_start;  // [npeers + 1] first global position of each output shard
+  uint32_t npeers;             // 0: local outputs keys_out / vals_out
+  uint32_t *peer_k[kMaxPeers];
+  uint32_t *peer_v[kMaxPeers];
 };
+
+// store of a scattered element at global position p: local, or (sharded) into
+// the window of the rank owning p (s_ps: the npeers + 1 shard starts in smem)
+template <bool PAIRS>
+__device__ __forceinline__ void kp_store(const KfArgs &a, const uint32_t *s_ps, uint32_t p,
+                                         uint32_t k, uint32_t v) {
+  uint32_t d = 0;
+#pragma unroll
+  for (uint32_t g = 1; g < kMaxPeers; ++g) d += (g < a.npeers && p >= s_ps[g]) ? 1u : 0u;
+  const uint32_t o = p - s_ps[d];
+  a.peer_k[d][o] = k;
+  if constexpr (PAIRS) a.peer_v[d][o] = v;
+}
 
 // CTA shapes by bucket class (warps W, windows per warp ITEMS; tile T = 32 W ITEMS),
 // chosen so that two (m <= 32, pairs) or three (keys, m > 32) CTAs fit in an SM's 228 KB:

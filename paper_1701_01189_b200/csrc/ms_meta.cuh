@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 // applied in program order.  Run in the postscan's own launch shape (512
 // threads, two CTAs per SM over the whole grid, every warp hammering its own
 // row of up to 256 counters with runs, random and skewed bucket patterns, 16
-// instructions back to back as in the rank loop); lane 0 of each warp replays
+// instructions back to back as in the rank loop; plain and packed 16-bit
+// counters as in ms_wide.cuh); lane 0 of each warp replays
 // the same increments sequentially with plain loads and stores, and every
 // returned value must equal the replay.  *flag is cleared if any differs.
 // ============================================================================
@@ -201,7 +202,8 @@ static __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t salt = (blockIdx.x * 131u + warp) * 0x9E3779B9u + pat * 0x85EBCA6Bu;
     const uint32_t mb = 1u + ((salt >> 7) & 255u);  // buckets in play: 1 .. 256
     const uint32_t kind = pat & 3u;                  // random / runs / 90 % hot / two values
-    for (uint32_t j = lane; j < 256u; j += 32u) row[j] = shadow[j] = (salt ^ j) & 0xFFFFu;
+    const bool packed = (pat & 4u) != 0u;            // two 16-bit counters per word (ms_wide.cuh)
+    for (uint32_t j = lane; j < 256u; j += 32u) row[j] = shadow[j] = (salt ^ j) & 0x7FFF7FFFu;
     uint32_t b[16], got[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -215,11 +217,23 @@ static __global__ void __launch_bounds__(kThreads, 2)
       ex[i * 32 + lane] = v;
     }
     __syncwarp();
+    if (packed) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) got[i] = atomicAdd(row + b[i], 1u);
+      for (int i = 0; i < 16; ++i) got[i] = atomicAdd(row + (b[i] >> 1), 1u << ((b[i] & 1u) << 4));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) got[i] = atomicAdd(row + b[i], 1u);
+    }
     __syncwarp();
-    if (lane == 0)
-      for (uint32_t e = 0; e < 512u; ++e) ex[e] = shadow[ex[e]]++;  // sequential replay
+    if (lane == 0) {  // sequential replay in (instruction, lane) order
+      for (uint32_t e = 0; e < 512u; ++e) {
+        const uint32_t v = ex[e];
+        const uint32_t w = packed ? v >> 1 : v;
+        const uint32_t old = shadow[w];
+        shadow[w] = old + (packed ? 1u << ((v & 1u) << 4) : 1u);
+        ex[e] = old;
+      }
+    }
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 16; ++i) ok &= got[i] == ex[i * 32 + lane];
@@ -274,6 +288,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ __align__(8) uint64_t placed[kStages];  // PROD: tile placed, 512 arrivals
   __shared__ __align__(8) uint64_t empty[kStages];   // PROD: stage free for a non-TMA tile
+  __shared__ uint32_t s_ps[kMaxPeers + 1];           // sharded: output shard starts
   const uint32_t m = bp.m, mS = SMALLM ? 2u : m;
   const uint32_t OS = kf_out_slots(T, m);
   const uint32_t MS = meta_stride(mS, W);
@@ -429,6 +444,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   // then forms base[b] + P[c][b] for its bucket lanes.  R is G m words, read
   // from L2 (11 MB in all at m = 32, G = 296).
   griddep_wait();  // KM complete: meta records and range histograms
+  if (a.npeers && tid <= a.npeers) s_ps[tid] = a.peer_start[tid];
   issue_meta(tile(0), 0);
   issue_meta(tile(1), 1);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(tile(j));
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       if (lane >= (uint32_t)o) incl += y;
     }
     if (lane < m) {
-      gbase = incl - tot + pre;
+      gbase = (a.gbase_ovr ? __ldg(a.gbase_ovr + lane) : incl - tot) + pre;
       if (c == 0 && warp == 0 && a.bucket_offsets) {
         a.bucket_offsets[lane] = incl - tot;
         if (lane == m - 1) a.bucket_offsets[m] = incl;
@@ -491,6 +507,12 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     const uint32_t tn = tile_n(t);
     const bool full = tn == T;
     uint32_t *tab = s_tab + st * 96u;
+    if constexpr (PROD) {
+      // a tile that is not TMA-loaded: the producer has finished the previous
+      // tile of this stage (its run table and its bulk stores' reads of the
+      // stage) before this tile's run table and placement overwrite them
+      if (!tma_tile && k >= 2) mbar_wait(&empty[st], a.use_tma ? 0u : ((k - 2) / kStages) & 1u);
+    }
 
     // ---- per-warp setup from the meta record (lane b = bucket b) -------------
     // slot of this warp's first bucket-b key = S[b][warp] (+ run padding adj[b]
@@ -519,9 +541,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       mrow1[lane] = 0u;
     }
     __syncwarp();
-    if constexpr (PROD) {  // the stage's previous tile has been read by its bulk stores
-      if (!tma_tile && k >= 2) mbar_wait(&empty[st], a.use_tma ? 0u : ((k - 2) / kStages) & 1u);
-    }
 
     // ---- rank and place (Eq.4 term 1 + this warp's running slot) -------------
     bool derr = false;
@@ -689,6 +708,12 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       for (int i = 0; i < ITEMS; ++i) kk[i] = s_stage[s0 + 32 * i];
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * i;
+      if (a.npeers) {  // sharded: into the owning rank's window (KP)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+          if (full || s0 + 32 * i < tn)
+            kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[OS + s0 + 32 * i] : 0u);
+      } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i)
         if (full || s0 + 32 * i < tn) a.keys_out[pos[i]] = kk[i];
@@ -698,6 +723,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i)
           if (full || s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
+      }
       }
       // ---- refill the stage of tile t-1 with tile t+2 (its loads and stores
       // finished before this tile's barrier)

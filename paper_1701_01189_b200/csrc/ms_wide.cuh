@@ -1,0 +1,472 @@
+// ms_wide.cuh -- the two-kernel pipeline of ms_meta.cuh widened to 32 < m <= 256
+// buckets (the m = 64/128/256 multisplits of configs[2] and every 8-bit pass of
+// the radix sort, configs[3]).
+//
+//   KMW km_meta_wide (prescan, P:534-535 extended): 16 counting warps count one
+//       512-key slice each of every 8192-key tile into warp-private counters
+//       (32-bit: same-address increments of one value merge in the shared-
+//       memory atomic unit, so a 90 % hot bucket costs nothing); one scan warp turns them into tile meta records
+//       S[w][b] = sum_{b'<b} h_b' + sum_{w'<w} c_{w',b}  (Eq.4 terms 2-3,
+//       P:952-955), stored as 16-bit slot bases, and accumulates the range
+//       histograms R[c][b] (the level-0 column of Eq.3).  For pairs the KF tile
+//       is 4096 elements (8 warp slices), so a KM tile yields two records.
+//   KR  kr_level0_scan (ms_kernels.cuh): P[c][b] = sum_{c'<c} R[c'][b], totals.
+//   KFW kf_meta_wide (postscan): persistent CTA per level-0 range,
+//       tiles in order; each warp takes its slot bases from its record row,
+//       ranks its keys (Eq.4 term 1) by lane-ordered increments of packed
+//       16-bit running slots (reading R23), places them in shared memory in
+//       place, one barrier, then the coalesced per-element scatter.
+//
+// Why (profiles/r02/dram0_*, smem_ubench): at m = 256 the single-kernel
+// postscan (kf_fused: count pass + block scan of the m x W counts + rank +
+// reorder) spends 16.8 shared-memory wavefronts per 32 keys and reaches
+// 2.2-2.6 TB/s; moving the count pass and the scan into the prescan (whose
+// shared-memory pipe is idle while it streams the keys) leaves the postscan
+// one atomic, one store and two loads per key.  The price is the records:
+// 2 B per key written and read at m = 256 keys (1 B per pair), which the
+// paper's recompute-instead-of-store choice (P:778 footnote) avoided on a GPU
+// whose postscan was not the bottleneck.
+//
+// Buckets are laid out blocked: lane l owns buckets NB*l .. NB*l+NB-1, and the
+// records, counters and range histograms use the padded width mP = 32 NB
+// (buckets >= m are empty).
+#pragma once
+#include "ms_meta.cuh"
+
+namespace ms {
+
+__host__ __device__ constexpr uint32_t wide_nb(uint32_t m) {
+  return m <= 64 ? 2u : (m <= 128 ? 4u : 8u);
+}
+// KF tile and its warp count: keys 16 warps x 16 windows, pairs 8 x 16
+__host__ __device__ constexpr uint32_t wide_kw(bool pairs) { return pairs ? 8u : 16u; }
+__host__ __device__ constexpr uint32_t wide_tile(bool pairs) { return 32u * 16u * wide_kw(pairs); }
+// record: KW rows of mP 16-bit slot bases
+__host__ __device__ constexpr uint32_t wide_rec_words(bool pairs, uint32_t nb) {
+  return wide_kw(pairs) * 32u * nb / 2u;
+}
+constexpr uint32_t kWideKmTile = 8192;  // KM tile (16 slices of 512 keys)
+// KM TMA ring depth: 3 tiles, 2 at m > 128 (32-bit warp counters of 256
+// buckets take 32 KB; two 32 KB tiles in flight per CTA, two CTAs per SM, are
+// still far more than the bytes in flight the HBM latency needs)
+__host__ __device__ constexpr uint32_t kmw_stages(uint32_t nb) { return nb == 8 ? 2u : 3u; }
+__host__ __device__ inline size_t kmw_smem_bytes(uint32_t nb) {
+  return (kmw_stages(nb) * kWideKmTile + 2u * kWarps * 32u * nb) * 4u;
+}
+__host__ __device__ inline size_t kfw_smem_bytes(bool pairs, uint32_t nb) {
+  const uint32_t T = wide_tile(pairs);
+  return (3u * T * (pairs ? 2u : 1u) + wide_kw(pairs) * 16u * nb + 2u * 32u * nb) * 4u;
+}
+
+template <int NB>
+struct WideVec;  // NB/2 packed words
+template <> struct WideVec<2> { using T = uint32_t; };
+template <> struct WideVec<4> { using T = uint2; };
+template <> struct WideVec<8> { using T = uint4; };
+
+// NB consecutive 32-bit words of shared memory (16-byte vector accesses)
+template <int NB>
+__device__ __forceinline__ void ld_words(const uint32_t *p, uint32_t (&u)[NB]) {
+  if constexpr (NB == 2) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
+    u[0] = v.x;
+    u[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NB / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4 *>(p)[q];
+      u[4 * q] = v.x;
+      u[4 * q + 1] = v.y;
+      u[4 * q + 2] = v.z;
+      u[4 * q + 3] = v.w;
+    }
+  }
+}
+template <int NB>
+__device__ __forceinline__ void st_zero_words(uint32_t *p) {
+  if constexpr (NB == 2) {
+    *reinterpret_cast<uint2 *>(p) = make_uint2(0u, 0u);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NB / 4; ++q) reinterpret_cast<uint4 *>(p)[q] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+template <int NB>
+__device__ __forceinline__ void wide_unpack(const typename WideVec<NB>::T &v, uint32_t (&w)[NB / 2]) {
+  if constexpr (NB == 2) {
+    w[0] = v;
+  } else if constexpr (NB == 4) {
+    w[0] = v.x;
+    w[1] = v.y;
+  } else {
+    w[0] = v.x;
+    w[1] = v.y;
+    w[2] = v.z;
+    w[3] = v.w;
+  }
+}
+template <int NB>
+__device__ __forceinline__ typename WideVec<NB>::T wide_pack(const uint32_t (&w)[NB / 2]) {
+  if constexpr (NB == 2) {
+    return w[0];
+  } else if constexpr (NB == 4) {
+    return make_uint2(w[0], w[1]);
+  } else {
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// ============================================================================
+// KMW.  CTA c handles KM tiles [c*K, min(LM, (c+1)*K)) of 8192 keys; warp w of
+// the 16 counting warps counts slice w (keys [t*8192 + 512 w, +512)).
+// ============================================================================
+template <int KIND, int NB, bool PAIRS>
+__global__ void __launch_bounds__(kThreads + 32, 2)
+    km_meta_wide(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
+                 uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
+                 uint32_t num_kf_tiles, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  constexpr uint32_t W = kWarps, SL = 512, T = kWideKmTile, KS = kmw_stages(NB);
+  constexpr uint32_t HW = NB / 2;                 // packed record words per lane per row
+  constexpr uint32_t RW = 16u * NB;               // packed record words per row (mP / 2)
+  constexpr uint32_t MP = 32u * NB;               // counters per warp row
+  constexpr uint32_t KW = wide_kw(PAIRS);         // warp rows per record
+  constexpr uint32_t REC = wide_rec_words(PAIRS, NB);
+  using V = typename WideVec<NB>::T;
+  extern __shared__ __align__(128) uint32_t kmw_smem[];  // stages [KS][T] | cnt[2][W][MP]
+  __shared__ __align__(8) uint64_t full[KS];
+  __shared__ __align__(8) uint64_t cfull[2];
+  __shared__ __align__(8) uint64_t cempty[2];
+  griddep_launch_dependents();
+  uint32_t *cnt = kmw_smem + KS * T;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (blockIdx.x == 0 && tid == 0) hdr[0] = 0u;
+  for (uint32_t i = tid; i < 2 * W * MP; i += blockDim.x) cnt[i] = 0u;
+  const uint32_t t0 = blockIdx.x * tiles_per_cta;
+  const uint32_t t1 = min(num_tiles, t0 + tiles_per_cta);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0);
+  auto via_tma = [&](uint32_t t) { return aligned && (uint64_t)(t + 1) * T <= n; };
+  if (tid == 0) {
+    for (uint32_t i = 0; i < KS; ++i) mbar_init(&full[i], 1);
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init(&cfull[i], kThreads);
+      mbar_init(&cempty[i], 32);
+    }
+  }
+  __syncthreads();
+
+  if (warp == W) {
+    // ============================ scan warp ===================================
+    auto issue = [&](uint32_t t, uint32_t st) {
+      if (lane == 0 && t < t1 && via_tma(t)) {
+        mbar_arrive_expect_tx(&full[st], T * 4u);
+        tma_load_1d(kmw_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], policy_evict_first());
+      }
+    };
+    for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
+    uint32_t running[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) running[j] = 0u;
+    uint32_t k = 0;
+    for (uint32_t t = t0; t < t1; ++t, ++k) {
+      const uint32_t p = k & 1u;
+      mbar_wait(&cfull[p], (k >> 1) & 1u);
+      if (lane == 0) fence_proxy_async_smem();
+      issue(t + KS, k % KS);
+      uint32_t *c = cnt + p * W * MP;
+#pragma unroll 1
+      for (uint32_t half = 0; half < W / KW; ++half) {
+        // pass 1: tile (or half-tile) count h of this lane's buckets
+        uint32_t h[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) h[j] = 0u;
+#pragma unroll 4
+        for (uint32_t w = 0; w < KW; ++w) {
+          uint32_t x[NB];
+          ld_words<NB>(c + (half * KW + w) * MP + lane * NB, x);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) h[j] += x[j];
+        }
+        // exclusive scan over the buckets (in-lane prefix + warp scan of lane sums)
+        uint32_t tb[NB], s = 0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          tb[j] = s;
+          s += h[j];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          tb[j] += incl - s;
+          running[j] += h[j];
+        }
+        // pass 2: S[w][b] = tb[b] + sum_{w'<w} c_{w',b}; zero the counters
+        const uint32_t tf = t * (W / KW) + half;  // KF tile of this record
+        uint32_t *rec = meta + (size_t)tf * REC;
+#pragma unroll 2
+        for (uint32_t w = 0; w < KW; ++w) {
+          uint32_t *cw = c + (half * KW + w) * MP + lane * NB;
+          uint32_t x[NB], o[HW];
+          ld_words<NB>(cw, x);
+#pragma unroll
+          for (int i = 0; i < (int)HW; ++i) {
+            o[i] = (tb[2 * i] & 0xFFFFu) | (tb[2 * i + 1] << 16);
+            tb[2 * i] += x[2 * i];
+            tb[2 * i + 1] += x[2 * i + 1];
+          }
+          st_zero_words<NB>(cw);
+          if (tf < num_kf_tiles) reinterpret_cast<V *>(rec + w * RW)[lane] = wide_pack<NB>(o);
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&cempty[p]);
+    }
+    uint32_t *r = R + (size_t)blockIdx.x * (32u * NB) + lane * NB;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) r[j] = running[j];
+    return;
+  }
+
+  // ============================ counting warps ================================
+  uint32_t k = 0;
+  for (uint32_t t = t0; t < t1; ++t, ++k) {
+    const uint32_t p = k & 1u, st = k % KS;
+    if (k >= 2) mbar_wait(&cempty[p], ((k - 2) >> 1) & 1u);
+    uint32_t *row = cnt + (p * W + warp) * MP;
+    if (via_tma(t)) {
+      mbar_wait(&full[st], (k / KS) & 1u);
+      const uint4 *v = reinterpret_cast<const uint4 *>(kmw_smem + st * T + warp * SL);
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = v[lane + 32u * (uint32_t)u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          atomicAdd(row + bucket_of<KIND>(k4[e], bp), 1u);
+        }
+      }
+    } else {  // ragged last tile / unaligned input
+      const uint64_t lo = (uint64_t)t * T + warp * SL;
+      const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
+      for (uint32_t i = (uint32_t)lo + lane; i < hi; i += 32u) {
+        atomicAdd(row + bucket_of<KIND>(__ldg(keys + i), bp), 1u);
+      }
+    }
+    mbar_arrive(&cfull[p]);
+  }
+}
+
+// ============================================================================
+// KFW: persistent CTA per level-0 range (KF tiles [c K, (c+1) K)), KW warps.
+//   iteration k (tile t): per-warp setup from the record row (loaded into
+//   registers with the tile's keys); rank + place in place; load tile t+1
+//   into registers; one barrier; per-element coalesced scatter of tile t;
+//   the last warp refills the stage of tile t-1 with tile t+2.
+// ============================================================================
+template <int KIND, bool PAIRS, int NB>
+__global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a, BucketParams bp) {
+  constexpr uint32_t W = wide_kw(PAIRS), NT = W * 32, ITEMS = 16;
+  constexpr uint32_t T = NT * ITEMS;
+  constexpr uint32_t kStages = 3, kPrefetch = 2;
+  constexpr uint32_t HW = NB / 2, RW = 16u * NB, MP = 32u * NB;
+  constexpr uint32_t REC = wide_rec_words(PAIRS, NB);
+  constexpr uint32_t SWD = T * (PAIRS ? 2u : 1u);  // words per stage
+  using V = typename WideVec<NB>::T;
+  extern __shared__ __align__(128) uint8_t kfw_raw[];
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ uint32_t s_ps[kMaxPeers + 1];  // sharded: output shard starts
+  uint32_t *stage0 = reinterpret_cast<uint32_t *>(kfw_raw);
+  uint32_t *s_row = stage0 + kStages * SWD;  // [W][RW] packed running slots
+  uint32_t *s_tab = s_row + W * RW;          // [2][MP] global minus tile offsets
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr uint32_t kProducer = NT - 32;
+
+  const uint32_t t0 = blockIdx.x * a.tiles_per_cta;
+  const uint32_t t1 = min(a.num_tiles, t0 + a.tiles_per_cta);
+  if (t0 >= t1) return;
+  const uint32_t nt = t1 - t0;
+  auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
+  auto via_tma = [&](uint32_t t) { return a.use_tma && tile_n(t) == T; };
+  auto issue = [&](uint32_t t, uint32_t st) {
+    if (tid == kProducer && t < t1 && via_tma(t)) {
+      uint32_t *dst = stage0 + st * SWD;
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
+      tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
+      if constexpr (PAIRS) tma_load_1d(dst + T, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
+    }
+  };
+  auto prefetch = [&](uint32_t t, bool meta) {
+    if (tid == kProducer && t < t1) {
+      const uint64_t pol = policy_evict_last();
+      if (via_tma(t)) {
+        prefetch_l2_bulk_hint(a.keys_in + (size_t)t * T, T * 4u, pol);
+        if constexpr (PAIRS) prefetch_l2_bulk_hint(a.vals_in + (size_t)t * T, T * 4u, pol);
+      }
+      if (meta) prefetch_l2_bulk_hint(a.meta + (size_t)t * REC, REC * 4u, pol);
+    }
+  };
+  if (tid == 0)
+    for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
+  __syncthreads();
+  issue(t0, 0);
+  issue(t0 + 1, 1);
+  for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, false);
+
+  uint32_t key[ITEMS];
+  uint32_t val[PAIRS ? ITEMS : 1];
+  uint32_t mrow[HW], mrow0[HW];  // this warp's record row and row 0 (packed 16-bit)
+  const uint32_t wbase = warp * (ITEMS * 32);
+  auto load_tile = [&](uint32_t t, uint32_t k) {
+    const uint32_t st = k % kStages;
+    const uint32_t *s = stage0 + st * SWD;
+    const uint32_t tn = tile_n(t);
+    const uint32_t *rec = a.meta + (size_t)t * REC;
+    wide_unpack<NB>(reinterpret_cast<const V *>(rec + warp * RW)[lane], mrow);
+    wide_unpack<NB>(reinterpret_cast<const V *>(rec)[lane], mrow0);
+    if (via_tma(t)) {
+      mbar_wait(&bar[st], (k / kStages) & 1u);
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) key[i] = s[wbase + 32 * i + lane];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int i = 0; i < (int)ITEMS; ++i) val[i] = s[T + wbase + 32 * i + lane];
+      }
+    } else {
+      const size_t g = (size_t)t * T;
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) {
+        const uint32_t e = wbase + 32 * i + lane;
+        key[i] = e < tn ? __ldg(a.keys_in + g + e) : 0u;
+        if constexpr (PAIRS) val[i] = e < tn ? __ldg(a.vals_in + g + e) : 0u;
+      }
+    }
+  };
+
+  // ---- level-0 offsets (Eq.3 terms 1-2): KR's column prefix P[c][b] and the
+  // bucket totals; base[b] = exclusive scan of the totals
+  griddep_wait();  // KM and KR complete
+  if (a.npeers && tid <= a.npeers) s_ps[tid] = a.peer_start[tid];
+  for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, true);
+  uint32_t grun[NB];  // next global position of each bucket of this lane in this range
+  {
+    const uint32_t c = blockIdx.x;
+    uint32_t tot[NB], s = 0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      tot[j] = __ldg(a.Tot + lane * NB + j);
+      grun[j] = s;
+      s += tot[j];
+    }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      grun[j] += incl - s;
+      const uint32_t b = lane * NB + j;
+      if (a.gbase_ovr) grun[j] = b < bp.m ? __ldg(a.gbase_ovr + b) : 0u;
+      if (c == 0 && warp == 0 && a.bucket_offsets) {
+        if (b < bp.m) a.bucket_offsets[b] = grun[j];
+        if (b + 1 == bp.m) a.bucket_offsets[bp.m] = grun[j] + tot[j];
+      }
+      grun[j] += __ldg(a.R + (size_t)c * MP + b);
+    }
+  }
+  load_tile(t0, 0);
+  __syncthreads();  // every warp holds tile t0 in registers before any places into its stage
+
+  uint32_t *brow = s_row + warp * RW;
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint32_t t = t0 + k;
+    const uint32_t st = k % kStages;
+    uint32_t *s_stage = stage0 + st * SWD;
+    const uint32_t tn = tile_n(t);
+    uint32_t *tab = s_tab + (k & 1u) * MP;
+
+    // ---- per-warp setup: running slots of this warp's buckets; the tile's
+    // global offsets (Eq.3 term 3: grun accumulates the range's earlier tiles)
+    {
+      uint32_t tb[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) tb[j] = (mrow0[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+      const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, tb[0], 1);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const uint32_t te = j + 1 < NB ? tb[j + 1] : (lane < 31 ? nxt : tn);
+        if (warp == W - 1) tab[lane * NB + j] = grun[j] - tb[j];
+        grun[j] += te - tb[j];
+      }
+      reinterpret_cast<V *>(brow)[lane] = wide_pack<NB>(mrow);
+    }
+    __syncwarp();
+
+    // ---- rank and place: slot = lane-ordered increment of the packed 16-bit
+    // running slot of the key's bucket (Eq.4 term 1, reading R23)
+    bool derr = false;
+#pragma unroll
+    for (int i = 0; i < (int)ITEMS; ++i) {
+      if (wbase + (uint32_t)i * 32u >= tn) break;  // warp-uniform: past the tail
+      const bool valid = wbase + (uint32_t)i * 32u + lane < tn;
+      const uint32_t b = bucket_of<KIND>(key[i], bp);
+      if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+      if (valid) {
+        const uint32_t sh = (b & 1u) << 4;
+        const uint32_t slot = (atomicAdd(brow + (b >> 1), 1u << sh) >> sh) & 0xFFFFu;
+        s_stage[slot] = key[i];
+        if constexpr (PAIRS) s_stage[T + slot] = val[i];
+      }
+    }
+    if constexpr (KIND == kIdentity) {
+      if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
+    }
+    if (k + 1 < nt) load_tile(t + 1, k + 1);
+    __syncthreads();
+
+    // ---- coalesced scatter of tile t: slot s of bucket b -> tab[b] + s --------
+    {
+      const uint32_t s0 = wbase + lane;
+      uint32_t kk[ITEMS], pos[ITEMS];
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[s0 + 32 * i];
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * i;
+      if (a.npeers) {  // sharded: into the owning rank's window (KP)
+#pragma unroll
+        for (int i = 0; i < (int)ITEMS; ++i)
+          if (s0 + 32 * i < tn)
+            kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[T + s0 + 32 * i] : 0u);
+      } else {
+#pragma unroll
+        for (int i = 0; i < (int)ITEMS; ++i)
+          if (s0 + 32 * i < tn) a.keys_out[pos[i]] = kk[i];
+        if constexpr (PAIRS) {
+#pragma unroll
+          for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[T + s0 + 32 * i];
+#pragma unroll
+          for (int i = 0; i < (int)ITEMS; ++i)
+            if (s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
+        }
+      }
+    }
+    // ---- refill the stage of tile t-1 (read before this tile's barrier) with t+2
+    if (warp == W - 1) {
+      __syncwarp();
+      if (lane == 0) fence_proxy_async_smem();
+      issue(t + 2, (k + 2) % kStages);
+      prefetch(t + 2 + kPrefetch, true);
+    }
+  }
+}
+
+}  // namespace ms

@@ -92,25 +92,36 @@ k = gen.keys(3000, seed=1, kind=gen.IDENTITY, m=10)
 k[77] = 10
 ms.multisplit(d(k), None, bucket=ms.Identity(10))
 check("domain flag", ms.device_status() == lib.MS_ERR_KEY_DOMAIN)
-# KX merge (virtual ranks: the sharded plan + merge of 3 shards on one GPU)
-G, m = 3, 64
-ob = oracle.delta(m)
-shards = [gen.keys(20000 + 7 * r, seed=r, kind=gen.DELTA, m=m, delta=ob.delta) for r in range(G)]
-loc = [ms.multisplit(d(s), None, bucket=ms.Delta(m)) for s in shards]
-C = np.stack([np.diff(h(o).astype(np.int64)) for _, _, o in loc]).astype(np.uint64)
-ek, _, _ = oracle.multisplit(np.concatenate(shards), ob)
-out, pos = [], 0
-for r in range(G):
-    plan = sharded.shard_plan(C, r)
-    parts = []
-    for s in range(G):
-        sp = sharded.shard_plan(C, s)
-        lo, cnt = int(sp["send_displs"][r]), int(sp["send_counts"][r])
-        parts.append(loc[s][0][lo:lo + cnt])
-    rk = torch.cat(parts)
-    ko, _ = sharded._cuda_merge(rk, None, ms.Delta(m), plan["recv_displs"], plan["merge_offsets"], G)
-    out.append(h(ko))
-check("shard merge", np.array_equal(np.concatenate(out), ek))
+# sharded: the fused KP path (ms_shard_prescan / ms_shard_scatter) with 3 virtual
+# ranks, and the NCCL path's plan + KX merge (ms_shard_merge_keys)
+import ctypes  # noqa: E402
+for G, m in ((3, 16), (3, 64)):
+    ob = oracle.delta(m)
+    shards = [gen.keys(20000 + 7 * r, seed=r, kind=gen.DELTA, m=m, delta=ob.delta) for r in range(G)]
+    vals = [gen.values(s.size, seed=r) for r, s in enumerate(shards)]
+    ok, ov, _ = sharded.virtual_ranks([d(s) for s in shards], [d(v) for v in vals], ms.Delta(m))
+    ek, ev, _ = oracle.multisplit(np.concatenate(shards), ob, np.concatenate(vals))
+    check(f"kp m{m}", np.array_equal(np.concatenate([h(x) for x in ok]), ek) and
+          np.array_equal(np.concatenate([h(x) for x in ov]), ev))
+    loc = [ms.multisplit(d(s), None, bucket=ms.Delta(m)) for s in shards]
+    C = np.stack([np.diff(h(o).astype(np.int64)) for _, _, o in loc]).astype(np.uint64)
+    out = []
+    for r in range(G):
+        plan = sharded.shard_plan(C, r)
+        parts = []
+        for q in range(G):
+            sp = sharded.shard_plan(C, q)
+            lo, cnt = int(sp["send_displs"][r]), int(sp["send_counts"][r])
+            parts.append(loc[q][0][lo:lo + cnt])
+        rk = torch.cat(parts)
+        starts = d(np.append(plan["recv_displs"], rk.numel()).astype(np.uint32))
+        offs = d(plan["merge_offsets"])
+        ko = torch.empty_like(rk)
+        fn = ms.Delta(m).c()
+        lib.check(lib.load().ms_shard_merge_keys(rk.data_ptr(), rk.numel(), ctypes.byref(fn), starts.data_ptr(),
+                                                 offs.data_ptr(), G, ko.data_ptr(), None))
+        out.append(h(ko))
+    check(f"shard merge m{m}", np.array_equal(np.concatenate(out), ek))
 # histogram
 x = gen.floats(70001, 5)
 spl = gen.splitters(37, 5)

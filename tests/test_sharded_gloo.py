@@ -1,9 +1,11 @@
 """Host logic of the sharded multisplit on CPU: the plan
-(ms_shard_plan, C host code in libms) checked for consistency, and the whole
-orchestration (all-gather of counts, plan, all-to-all-v, merge placement) run
-by world_size 2 and 3 gloo process groups.  The GPU steps (local multisplit,
-merge kernel) are replaced here by test stand-ins built on the oracle; the
-CUDA kernels themselves are covered by tests/test_gpu_sharded.py."""
+(ms_shard_plan, the C host code libms's NCCL path runs) checked for
+consistency, and the exchange it drives (all-gather of counts, plan,
+all-to-all-v, merge placement) run by world_size 2 and 3 gloo process groups
+(sharded.exchange_reference).  The GPU steps (local multisplit, merge kernel)
+are replaced here by stand-ins built on the oracle; the library's own sharded
+calls (NCCL inside libms, fused KP scatter) are covered by
+tests/test_gpu_sharded.py."""
 import os
 import socket
 
@@ -72,7 +74,7 @@ def _worker(rank, world, port, sizes, m, kind, pairs, out_dir):
     hi = lo + sizes[rank]
     k = torch.from_numpy(keys[lo:hi].view(np.int32).copy())
     v = torch.from_numpy(vals[lo:hi].view(np.int32).copy()) if pairs else None
-    ko, vo, go = sharded.sharded_multisplit(k, v, bucket, local_op=oracle_local, merge_op=numpy_merge)
+    ko, vo, go = sharded.exchange_reference(k, v, bucket, oracle_local, numpy_merge)
     np.save(os.path.join(out_dir, f"k{rank}.npy"), ko.numpy().view(np.uint32))
     if pairs:
         np.save(os.path.join(out_dir, f"v{rank}.npy"), vo.numpy().view(np.uint32))
