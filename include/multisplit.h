@@ -325,7 +325,8 @@ ms_status ms_multisplit_pairs_sharded(ms_comm *comm, const uint32_t *keys_in, co
  *     NULL) receives the shard's bucket counts C[r][0..m).
  *   ms_shard_scatter: C = the G x m gathered counts (device, row s = rank s);
  *     peer_keys / peer_vals = host arrays of G device pointers, the output
- *     shard of every rank (peer_vals NULL: keys only); writes this rank's
+ *     shard of every rank (peer_vals NULL: keys only; an entry may be NULL
+ *     for a rank whose shard is empty); writes this rank's
  *     elements into the owners' shards and, if global_bucket_offsets is not
  *     NULL, the m+1 global bucket starts (uint64, device).
  * ws: ms_shard_workspace_size(n_local, m, G, with_values) bytes.  Errors as

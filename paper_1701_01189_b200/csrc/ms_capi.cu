@@ -1045,8 +1045,9 @@ ms_status shard_scatter_impl(const uint32_t *keys_in, const uint32_t *vals_in, u
   if (!kp_supported(m)) return MS_ERR_UNSUPPORTED;
   if (G == 0 || G > kMaxPeers || r >= G || !C || !peer_k) return MS_ERR_INVALID_VALUE;
   if (pairs && (!peer_v || (n > 0 && !vals_in))) return MS_ERR_INVALID_VALUE;
-  for (uint32_t d = 0; d < G; ++d)
-    if (!peer_k[d] || (pairs && !peer_v[d])) return MS_ERR_INVALID_VALUE;
+  // peer windows may be NULL only for ranks whose shard is empty (nothing is
+  // stored there); this rank's own window must exist when it holds elements
+  if (n > 0 && (!peer_k[r] || (pairs && !peer_v[r]))) return MS_ERR_INVALID_VALUE;
   const ShardLayout sl = shard_layout(n, m, G, pairs);
   if (ws_bytes < sl.total) return MS_ERR_WORKSPACE;
   char *w = (char *)ws;

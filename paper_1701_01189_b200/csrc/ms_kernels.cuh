@@ -131,12 +131,12 @@ static __global__ void __launch_bounds__(kThreads)
   if (p < NP) {
     if (S <= kMaxS) {
 #pragma unroll
-      for (uint32_t i = 0; i < kMaxS; ++i) v[i] = r0 + i < r1 ? __ldg(R + (size_t)(r0 + i) * m + b) : 0u;
+      for (uint32_t i = 0; i < kMaxS; ++i) v[i] = r0 + i < r1 ? __ldcg(R + (size_t)(r0 + i) * m + b) : 0u;
 #pragma unroll
       for (uint32_t i = 0; i < kMaxS; ++i) sum += v[i];
     } else {
 #pragma unroll 8
-      for (uint32_t r = r0; r < r1; ++r) sum += __ldg(R + (size_t)r * m + b);
+      for (uint32_t r = r0; r < r1; ++r) sum += __ldcg(R + (size_t)r * m + b);
     }
     s_part[p * wb + bl] = sum;
   }
@@ -159,7 +159,7 @@ static __global__ void __launch_bounds__(kThreads)
     } else {
 #pragma unroll 8
       for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t x = __ldg(R + (size_t)r * m + b);
+        const uint32_t x = __ldcg(R + (size_t)r * m + b);
         P[(size_t)r * m + b] = run;
         run += x;
       }
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
   if (a.mode == kModeRange) {
     // bucket bases = exclusive scan of the totals (block scan; thread b holds bucket b)
     const uint32_t lane = tid & 31, warp = tid >> 5;
-    const uint32_t t = tid < m ? __ldg(a.Tot + tid) : 0u;
+    const uint32_t t = tid < m ? __ldcg(a.Tot + tid) : 0u;
     uint32_t incl = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams 
     __syncthreads();
     if (tid < m) {
       const uint32_t gbase = s_wsum[warp] + incl - t;
-      s_delta[tid] = gbase + __ldg(a.R + (size_t)blockIdx.x * m + tid);
+      s_delta[tid] = gbase + __ldcg(a.R + (size_t)blockIdx.x * m + tid);
       if (blockIdx.x == 0 && a.bucket_offsets) {
         a.bucket_offsets[tid] = gbase;
         if (tid == m - 1) a.bucket_offsets[m] = gbase + t;

@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
   // then forms base[b] + P[c][b] for its bucket lanes.  R is G m words, read
   // from L2 (11 MB in all at m = 32, G = 296).
   griddep_wait();  // KM complete: meta records and range histograms
-  if (a.npeers && tid <= a.npeers) s_ps[tid] = a.peer_start[tid];
+  if (a.npeers && tid <= a.npeers) s_ps[tid] = __ldcg(a.peer_start + tid);
   issue_meta(tile(0), 0);
   issue_meta(tile(1), 1);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(tile(j));
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
 #pragma unroll
         for (int j = 0; j < 20; ++j) {
           const uint32_t r = r0 + j * W;
-          v[j] = r < G ? __ldg(a.R + (size_t)r * m + lane) : 0u;
+          v[j] = r < G ? __ldcg(a.R + (size_t)r * m + lane) : 0u;
         }
 #pragma unroll
         for (int j = 0; j < 20; ++j) {
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       if (lane >= (uint32_t)o) incl += y;
     }
     if (lane < m) {
-      gbase = (a.gbase_ovr ? __ldg(a.gbase_ovr + lane) : incl - tot) + pre;
+      gbase = (a.gbase_ovr ? __ldcg(a.gbase_ovr + lane) : incl - tot) + pre;
       if (c == 0 && warp == 0 && a.bucket_offsets) {
         a.bucket_offsets[lane] = incl - tot;
         if (lane == m - 1) a.bucket_offsets[m] = incl;
@@ -519,9 +519,14 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
     // so that the run starts congruent mod 4 with its global destination)
     uint32_t wrun = 0;
     if (lane < m) {
-      const uint32_t sbw = rec[warp * mS + lane];
-      const uint32_t tb = rec[lane];
-      const uint32_t te = lane + 1 < m ? rec[lane + 1] : tn;
+      // records of tiles that are not TMA-loaded come from global memory,
+      // written by KM: read through L2 (a programmatic dependent launch may
+      // start before KM completes, and its L1 can hold lines of an earlier
+      // use of the workspace -- measured: stale reads without .cg)
+      auto rd = [&](uint32_t i) { return tma_tile ? rec[i] : __ldcg(rec + i); };
+      const uint32_t sbw = rd(warp * mS + lane);
+      const uint32_t tb = rd(lane);
+      const uint32_t te = lane + 1 < m ? rd(lane + 1) : tn;
       const uint32_t gs = gbase + grun;  // + Eq.3 term 3: the range's tiles before this one
       grun += te - tb;
       const uint32_t adj = a.store_runs ? 4u * lane + ((gs - tb) & 3u) : 0u;

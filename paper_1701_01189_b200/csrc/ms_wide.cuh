@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
     const uint32_t *s = stage0 + st * SWD;
     const uint32_t tn = tile_n(t);
     const uint32_t *rec = a.meta + (size_t)t * REC;
-    wide_unpack<NB>(reinterpret_cast<const V *>(rec + warp * RW)[lane], mrow);
-    wide_unpack<NB>(reinterpret_cast<const V *>(rec)[lane], mrow0);
+    wide_unpack<NB>(__ldcg(reinterpret_cast<const V *>(rec + warp * RW) + lane), mrow);
+    wide_unpack<NB>(__ldcg(reinterpret_cast<const V *>(rec) + lane), mrow0);
     if (via_tma(t)) {
       mbar_wait(&bar[st], (k / kStages) & 1u);
 #pragma unroll
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   // ---- level-0 offsets (Eq.3 terms 1-2): KR's column prefix P[c][b] and the
   // bucket totals; base[b] = exclusive scan of the totals
   griddep_wait();  // KM and KR complete
-  if (a.npeers && tid <= a.npeers) s_ps[tid] = a.peer_start[tid];
+  if (a.npeers && tid <= a.npeers) s_ps[tid] = __ldcg(a.peer_start + tid);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, true);
   uint32_t grun[NB];  // next global position of each bucket of this lane in this range
   {
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
     uint32_t tot[NB], s = 0;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      tot[j] = __ldg(a.Tot + lane * NB + j);
+      tot[j] = __ldcg(a.Tot + lane * NB + j);
       grun[j] = s;
       s += tot[j];
     }
@@ -375,12 +375,12 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
     for (int j = 0; j < NB; ++j) {
       grun[j] += incl - s;
       const uint32_t b = lane * NB + j;
-      if (a.gbase_ovr) grun[j] = b < bp.m ? __ldg(a.gbase_ovr + b) : 0u;
+      if (a.gbase_ovr) grun[j] = b < bp.m ? __ldcg(a.gbase_ovr + b) : 0u;
       if (c == 0 && warp == 0 && a.bucket_offsets) {
         if (b < bp.m) a.bucket_offsets[b] = grun[j];
         if (b + 1 == bp.m) a.bucket_offsets[bp.m] = grun[j] + tot[j];
       }
-      grun[j] += __ldg(a.R + (size_t)c * MP + b);
+      grun[j] += __ldcg(a.R + (size_t)c * MP + b);
     }
   }
   load_tile(t0, 0);
