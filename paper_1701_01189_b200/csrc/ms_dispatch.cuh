@@ -172,6 +172,11 @@ cudaError_t Launch<KIND>::fused_meta(bool pairs, const KfArgs &a, const BucketPa
   if (bp.m <= 2)
     return pairs ? kfm_go<KIND, true, true, kRankBallot>(a, bp, grid, s)
                  : kfm_go<KIND, false, true, kRankBallot>(a, bp, grid, s);
+  // m <= 4: ballots (measured faster than increments, which serialize on
+  // eight lanes per counter); otherwise increments where the probe held
+  if (bp.m <= 4)
+    return pairs ? kfm_go<KIND, true, false, kRankVote2>(a, bp, grid, s)
+                 : kfm_go<KIND, false, false, kRankVote2>(a, bp, grid, s);
   if (a.rank_inc)
     return pairs ? kfm_go<KIND, true, false, kRankInc>(a, bp, grid, s)
                  : kfm_go<KIND, false, false, kRankInc>(a, bp, grid, s);

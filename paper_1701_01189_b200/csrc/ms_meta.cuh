@@ -257,7 +257,16 @@ __host__ __device__ inline size_t kfm_smem_bytes(uint32_t m, bool pairs) {
 //   kRankMasks deterministic: peer masks by a shared-memory OR of the lane bit,
 //              taken and cleared by one atomic exchange per bucket lane, two
 //              windows in flight (Alg.3's peer masks).
-enum : int { kRankBallot = 0, kRankMasks = 7, kRankInc = 8 };
+//   kRankVote2 deterministic, for 2 < m <= 4: Alg.3's ballots
+//              (P:909-930), one __ballot_sync per bit of the bucket id; the
+//              peer mask of a key is the AND of the (possibly inverted)
+//              ballots, and lane j forms bucket j's mask the same way to
+//              advance the warp's running slot.  No shared-memory atomics: at
+//              m = 4 eight lanes share each counter and the increments
+//              serialize in the atomic unit (profiles/r02; measured 337 -> 396
+//              Gkeys/s at m = 4; three ballots at m = 8 were slower than
+//              increments, 335 vs 371).
+enum : int { kRankBallot = 0, kRankVote2 = 2, kRankMasks = 7, kRankInc = 8 };
 
 // ============================================================================
 // KF (meta mode): persistent CTA per level-0 range, tiles in order; 16
@@ -557,6 +566,8 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         uint32_t *brow = mrow0;
         if (lane < m) brow[lane] = wrun;
         __syncwarp();
+        // (one increment, then its placement: issuing all increments first was
+        // measured slower at m = 8 / 16, where more lanes share a counter)
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           const bool valid = FULL || wbase + (uint32_t)i * 32u + lane < tn;
@@ -597,6 +608,31 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
           if constexpr (PAIRS) {
             s_stage[OS + slot0] = val[i];
             s_stage[OS + slot1] = val[i + 1];
+          }
+        }
+        return;
+      }
+      if constexpr (RANK == kRankVote2) {
+        constexpr int LOGM = 2;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const bool valid = FULL || wbase + (uint32_t)i * 32u + lane < tn;
+          if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;  // warp-uniform
+          const uint32_t b = bucket_of<KIND>(key[i], bp);
+          if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+          const uint32_t vm = FULL ? 0xFFFFFFFFu : __ballot_sync(0xFFFFFFFFu, valid);
+          uint32_t peers = vm, mine = vm;
+#pragma unroll
+          for (int q = 0; q < LOGM; ++q) {
+            const uint32_t bq = __ballot_sync(0xFFFFFFFFu, valid && ((b >> q) & 1u));
+            peers &= ((b >> q) & 1u) ? bq : ~bq;
+            mine &= ((lane >> q) & 1u) ? bq : ~bq;
+          }
+          const uint32_t slot = __shfl_sync(0xFFFFFFFFu, wrun, b) + __popc(peers & lt);
+          wrun += __popc(mine);  // lanes >= m: buckets that never occur
+          if (valid) {
+            s_stage[slot] = key[i];
+            if constexpr (PAIRS) s_stage[OS + slot] = val[i];
           }
         }
         return;
@@ -706,6 +742,12 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       // ---- next tile's keys into registers before the barrier -----------------
       if (k + 1 < nt) load_tile(tile(k + 1), k + 1);
       named_barrier_sync(1, NT);
+      // ---- refill the stage of tile t-1 with tile t+2 (every warp finished
+      // tile t-1's scatter before this barrier): a whole scatter earlier
+      if (tid == kProducer) {
+        fence_proxy_async_smem();
+        issue(k + 2, (k + 2) % kStages);
+      }
       // ---- coalesced scatter of tile t: slot s of bucket b -> delta[b] + s ----
       const uint32_t s0 = wbase + lane;
       uint32_t kk[ITEMS], pos[ITEMS];
@@ -729,13 +771,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         for (int i = 0; i < ITEMS; ++i)
           if (full || s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
       }
-      }
-      // ---- refill the stage of tile t-1 with tile t+2 (its loads and stores
-      // finished before this tile's barrier)
-      if (warp == W - 1) {
-        __syncwarp();
-        if (lane == 0) fence_proxy_async_smem();
-        issue(k + 2, (k + 2) % kStages);
       }
     }
   }

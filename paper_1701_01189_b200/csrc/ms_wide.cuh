@@ -413,18 +413,37 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
 
     // ---- rank and place: slot = lane-ordered increment of the packed 16-bit
     // running slot of the key's bucket (Eq.4 term 1, reading R23)
+    // all increments of the warp first, then the placements: the increments
+    // are in flight together (the probe checks exactly this back-to-back form)
     bool derr = false;
+    if (tn == T) {
+      uint32_t slot[ITEMS];
 #pragma unroll
-    for (int i = 0; i < (int)ITEMS; ++i) {
-      if (wbase + (uint32_t)i * 32u >= tn) break;  // warp-uniform: past the tail
-      const bool valid = wbase + (uint32_t)i * 32u + lane < tn;
-      const uint32_t b = bucket_of<KIND>(key[i], bp);
-      if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
-      if (valid) {
-        const uint32_t sh = (b & 1u) << 4;
-        const uint32_t slot = (atomicAdd(brow + (b >> 1), 1u << sh) >> sh) & 0xFFFFu;
-        s_stage[slot] = key[i];
-        if constexpr (PAIRS) s_stage[T + slot] = val[i];
+      for (int i = 0; i < (int)ITEMS; ++i) {
+        const uint32_t b = bucket_of<KIND>(key[i], bp);
+        if constexpr (KIND == kIdentity) derr |= key_domain_error<KIND>(key[i], bp);
+        slot[i] = atomicAdd(brow + (b >> 1), 1u << ((b & 1u) << 4));
+        slot[i] = (slot[i] >> ((b & 1u) << 4)) & 0xFFFFu;
+      }
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) s_stage[slot[i]] = key[i];
+      if constexpr (PAIRS) {
+#pragma unroll
+        for (int i = 0; i < (int)ITEMS; ++i) s_stage[T + slot[i]] = val[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) {
+        if (wbase + (uint32_t)i * 32u >= tn) break;  // warp-uniform: past the tail
+        const bool valid = wbase + (uint32_t)i * 32u + lane < tn;
+        const uint32_t b = bucket_of<KIND>(key[i], bp);
+        if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+        if (valid) {
+          const uint32_t sh = (b & 1u) << 4;
+          const uint32_t slot = (atomicAdd(brow + (b >> 1), 1u << sh) >> sh) & 0xFFFFu;
+          s_stage[slot] = key[i];
+          if constexpr (PAIRS) s_stage[T + slot] = val[i];
+        }
       }
     }
     if constexpr (KIND == kIdentity) {
@@ -432,6 +451,14 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
     }
     if (k + 1 < nt) load_tile(t + 1, k + 1);
     __syncthreads();
+    // ---- refill the stage of tile t-1 with tile t+2: every warp finished tile
+    // t-1's scatter before this barrier, so the copy starts a whole scatter
+    // earlier than after this tile's
+    if (tid == kProducer) {
+      fence_proxy_async_smem();
+      issue(t + 2, (k + 2) % kStages);
+      prefetch(t + 2 + kPrefetch, true);
+    }
 
     // ---- coalesced scatter of tile t: slot s of bucket b -> tab[b] + s --------
     {
@@ -446,6 +473,17 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
         for (int i = 0; i < (int)ITEMS; ++i)
           if (s0 + 32 * i < tn)
             kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[T + s0 + 32 * i] : 0u);
+      } else if (tn == T) {  // full tile: no per-element predicates
+        uint32_t *__restrict__ ko = a.keys_out;
+#pragma unroll
+        for (int i = 0; i < (int)ITEMS; ++i) ko[pos[i]] = kk[i];
+        if constexpr (PAIRS) {
+          uint32_t *__restrict__ vo = a.vals_out;
+#pragma unroll
+          for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[T + s0 + 32 * i];
+#pragma unroll
+          for (int i = 0; i < (int)ITEMS; ++i) vo[pos[i]] = kk[i];
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < (int)ITEMS; ++i)
@@ -458,13 +496,6 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
             if (s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
         }
       }
-    }
-    // ---- refill the stage of tile t-1 (read before this tile's barrier) with t+2
-    if (warp == W - 1) {
-      __syncwarp();
-      if (lane == 0) fence_proxy_async_smem();
-      issue(t + 2, (k + 2) % kStages);
-      prefetch(t + 2 + kPrefetch, true);
     }
   }
 }
