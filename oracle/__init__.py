@@ -25,7 +25,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "multisplit_oracle.c")
 _LIB = os.path.join(_HERE, "liborc.so")
 
-IDENTITY, DELTA, RADIX = 0, 1, 2
+IDENTITY, DELTA, RADIX, SPLITTERS = 0, 1, 2, 3
+MAX_M = 65536
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_KEY_DOMAIN = 0, 1, 2, 5
 
 
@@ -64,6 +65,11 @@ def _load():
         f32 = ctypes.c_float
         lib.orc_histogram_even.argtypes = [p, u64, u32, f32, f32, p]
         lib.orc_histogram_range.argtypes = [p, u64, u32, p, p]
+        lib.orc_validate_ex.argtypes = [u32, u32, u64, u32, u32, p]
+        lib.orc_bucket_ex.argtypes = [u32, u32, u64, u32, u32, p, u32, ctypes.POINTER(u32)]
+        lib.orc_multisplit_ex.argtypes = [p, p, p, p, u64, u32, u32, u64, u32, u32, p, p]
+        for f in (lib.orc_validate_ex, lib.orc_bucket_ex, lib.orc_multisplit_ex):
+            f.restype = ctypes.c_int
         for f in (lib.orc_validate, lib.orc_bucket, lib.orc_multisplit,
                   lib.orc_tile_histogram, lib.orc_radix_sort, lib.orc_histogram_even,
                   lib.orc_histogram_range):
@@ -73,10 +79,16 @@ def _load():
 
 
 class Bucket:
-    """Bucket identifier f(.): kind in {IDENTITY, DELTA, RADIX}."""
+    """Bucket identifier f(.): kind in {IDENTITY, DELTA, RADIX, SPLITTERS}."""
 
-    def __init__(self, kind: int, m: int, delta: int = 0, shift: int = 0, bits: int = 0):
+    def __init__(self, kind: int, m: int, delta: int = 0, shift: int = 0, bits: int = 0,
+                 splitters=None):
         self.kind, self.m, self.delta, self.shift, self.bits = kind, m, delta, shift, bits
+        self.splitters = None if splitters is None else _u32(splitters)
+
+    def extended(self) -> bool:
+        """Needs the extended entry points (splitters, or m beyond the paper's 256)."""
+        return self.kind == SPLITTERS or self.m > 256
 
     def args(self):
         return (self.kind, self.m, self.delta, self.shift, self.bits)
@@ -100,6 +112,13 @@ def radix(shift: int, bits: int) -> Bucket:
     return Bucket(RADIX, 1 << bits, shift=shift, bits=bits)
 
 
+def splitters(spl) -> Bucket:
+    """Splitter buckets (P:1110, reading R27): m-1 interior splitters s_1 < ... < s_{m-1};
+    f(u) = the j with s_j <= u < s_{j+1} (s_0 = 0, s_m = 2^32)."""
+    spl = _u32(spl)
+    return Bucket(SPLITTERS, spl.size + 1, splitters=spl)
+
+
 def _u32(a) -> np.ndarray:
     a = np.ascontiguousarray(a)
     if a.dtype != np.uint32:
@@ -113,25 +132,35 @@ def _ptr(a: np.ndarray | None):
 
 def bucket_of(fn: Bucket, u: int) -> int:
     b = ctypes.c_uint32(0)
-    st = _load().orc_bucket(*fn.args(), int(u) & 0xFFFFFFFF, ctypes.byref(b))
+    if fn.extended():
+        st = _load().orc_bucket_ex(*fn.args(), _ptr(fn.splitters), int(u) & 0xFFFFFFFF, ctypes.byref(b))
+    else:
+        st = _load().orc_bucket(*fn.args(), int(u) & 0xFFFFFFFF, ctypes.byref(b))
     if st:
         raise OracleError(st)
     return b.value
 
 
 def validate(fn: Bucket) -> int:
+    if fn.extended():
+        return _load().orc_validate_ex(*fn.args(), _ptr(fn.splitters))
     return _load().orc_validate(*fn.args())
 
 
 def multisplit(keys, fn: Bucket, values=None):
-    """Stable multisplit (Eq.1).  Returns (keys_out, values_out|None, offsets[m+1])."""
+    """Stable multisplit (Eq.1).  Returns (keys_out, values_out|None, offsets[m+1]).
+    Splitter buckets and m > 256 go through orc_multisplit_ex (same definition)."""
     keys = _u32(keys)
     n = keys.size
     vals = None if values is None else _u32(values)
     ko = np.empty(n, np.uint32)
     vo = None if vals is None else np.empty(n, np.uint32)
-    off = np.empty(fn.m + 1 if 1 <= fn.m <= 256 else 1, np.uint32)
-    st = _load().orc_multisplit(_ptr(keys), _ptr(vals), _ptr(ko), _ptr(vo), n, *fn.args(), _ptr(off))
+    off = np.empty(fn.m + 1 if 1 <= fn.m <= MAX_M else 1, np.uint32)
+    if fn.extended():
+        st = _load().orc_multisplit_ex(_ptr(keys), _ptr(vals), _ptr(ko), _ptr(vo), n, *fn.args(),
+                                       _ptr(fn.splitters), _ptr(off))
+    else:
+        st = _load().orc_multisplit(_ptr(keys), _ptr(vals), _ptr(ko), _ptr(vo), n, *fn.args(), _ptr(off))
     if st:
         raise OracleError(st)
     return ko, vo, off

@@ -16,11 +16,22 @@
  *                       f_k(u)=(u>>kr)&(2^r-1) (Sec.7.1).
  *                       Delta clamps to m-1 (reading R7);
  *                       identity with u>=m is a domain error (reading R8).
+ *                       Splitter buckets (Sec.6 "Bucket
+ *                       identification"): f(u) = the j with s_j <= u <
+ *                       s_{j+1}, where the caller gives the m-1 interior
+ *                       splitters s_1 < ... < s_{m-1} and s_0 = 0, s_m = 2^32
+ *                       are the ends of the uint32 key domain (DESIGN.md
+ *                       reading R27), found by a textbook upper-bound
+ *                       binary search (the search P:1110 names).
  *   orc_multisplit      stable multisplit = Eq.(1) (Sec.4.2):
  *                       p(i) = sum_{k<j} h_k + |{u_r in B_j : r < i}|,
  *                       computed as count -> exclusive scan -> stable
  *                       ascending scatter.  bucket_offsets has m+1 entries
- *                       (reading R2).
+ *                       (reading R2).  m <= 256 (the paper's scope).
+ *   orc_multisplit_ex   the same Eq.(1) for every bucket kind including
+ *                       splitters, and for m up to 65536 buckets (the m > 256
+ *                       regime of Sec.6.3): the definition does
+ *                       not depend on m, only the histogram array grows.
  *   orc_tile_histogram  the matrix H=[h_{j,l}] of Eq.(2) (Sec.4.3)
  *                       for L contiguous subproblems of T elements (last one
  *                       ragged), stored tile-major H[l*m + j].
@@ -52,7 +63,8 @@
 
 enum { ORC_OK = 0, ORC_ERR_INVALID = 1, ORC_ERR_UNSUPPORTED = 2,
        ORC_ERR_KEY_DOMAIN = 5 };
-enum { ORC_IDENTITY = 0, ORC_DELTA = 1, ORC_RADIX = 2 };
+enum { ORC_IDENTITY = 0, ORC_DELTA = 1, ORC_RADIX = 2, ORC_SPLITTERS = 3 };
+enum { ORC_MAX_M = 65536 };
 
 /* Validation rules of the bucket function. */
 int orc_validate(uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
@@ -122,6 +134,91 @@ int orc_multisplit(const uint32_t *keys_in, const uint32_t *vals_in,
     keys_out[p] = keys_in[i];
     if (vals_in && vals_out) vals_out[p] = vals_in[i];
   }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------- extended
+ * Every bucket kind (splitters included) and 1 <= m <= 65536.  RADIX digits
+ * may then be up to 16 bits wide.  spl: the m-1 interior splitters (may be
+ * NULL when m = 1 or the kind is not ORC_SPLITTERS). */
+int orc_validate_ex(uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+                    uint32_t bits, const uint32_t *spl) {
+  if (m < 1 || m > ORC_MAX_M) return ORC_ERR_UNSUPPORTED;
+  if (kind == ORC_IDENTITY) return ORC_OK;
+  if (kind == ORC_DELTA) return delta >= 1 ? ORC_OK : ORC_ERR_INVALID;
+  if (kind == ORC_RADIX) {
+    if (bits < 1 || bits > 16) return ORC_ERR_INVALID;
+    if ((uint64_t)shift + bits > 32) return ORC_ERR_INVALID;
+    if (m != (1u << bits)) return ORC_ERR_INVALID;
+    return ORC_OK;
+  }
+  if (kind == ORC_SPLITTERS) {
+    if (m > 1 && !spl) return ORC_ERR_INVALID;
+    for (uint32_t j = 1; j + 1 < m; ++j)  /* s_1 < s_2 < ... < s_{m-1} */
+      if (!(spl[j - 1] < spl[j])) return ORC_ERR_INVALID;
+    return ORC_OK;
+  }
+  return ORC_ERR_INVALID;
+}
+
+/* Splitter bucket: the number of interior splitters <= u (upper bound over
+ * s_1..s_{m-1}), i.e. the j with s_j <= u < s_{j+1} (reading R27). */
+static uint32_t orc_splitter_bucket(const uint32_t *spl, uint32_t m, uint32_t u) {
+  uint32_t lo = 0, hi = m - 1;  /* answer in [lo, hi]: count of spl[0..m-2] <= u */
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;  /* spl[mid] is s_{mid+1} */
+    if (spl[mid] <= u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+int orc_bucket_ex(uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+                  uint32_t bits, const uint32_t *spl, uint32_t u, uint32_t *b) {
+  if (kind == ORC_SPLITTERS) {
+    *b = orc_splitter_bucket(spl, m, u);
+    return ORC_OK;
+  }
+  if (kind == ORC_RADIX) {
+    *b = (uint32_t)(((uint64_t)u >> shift) & ((1ull << bits) - 1ull));
+    return ORC_OK;
+  }
+  return orc_bucket(kind, m, delta, shift, bits, u, b);
+}
+
+int orc_multisplit_ex(const uint32_t *keys_in, const uint32_t *vals_in,
+                      uint32_t *keys_out, uint32_t *vals_out, uint64_t n,
+                      uint32_t kind, uint32_t m, uint64_t delta, uint32_t shift,
+                      uint32_t bits, const uint32_t *spl, uint32_t *offsets) {
+  int st = orc_validate_ex(kind, m, delta, shift, bits, spl);
+  if (st) return st;
+  uint64_t *h = (uint64_t *)calloc(m, sizeof(uint64_t));
+  uint64_t *cur = (uint64_t *)calloc(m, sizeof(uint64_t));
+  if (!h || !cur) { free(h); free(cur); return ORC_ERR_INVALID; }
+  for (uint64_t i = 0; i < n; ++i) {  /* h_k */
+    uint32_t b;
+    st = orc_bucket_ex(kind, m, delta, shift, bits, spl, keys_in[i], &b);
+    if (st) { free(h); free(cur); return st; }
+    h[b] += 1;
+  }
+  uint64_t run = 0;                   /* sum_{k<j} h_k */
+  for (uint32_t j = 0; j < m; ++j) {
+    if (offsets) offsets[j] = (uint32_t)run;
+    cur[j] = run;
+    run += h[j];
+  }
+  if (offsets) offsets[m] = (uint32_t)run;
+  for (uint64_t i = 0; i < n; ++i) {  /* ascending i: |{u_r in B_j : r < i}| */
+    uint32_t b;
+    orc_bucket_ex(kind, m, delta, shift, bits, spl, keys_in[i], &b);
+    uint64_t p = cur[b]++;
+    keys_out[p] = keys_in[i];
+    if (vals_in && vals_out) vals_out[p] = vals_in[i];
+  }
+  free(h);
+  free(cur);
   return ORC_OK;
 }
 
