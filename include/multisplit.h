@@ -23,7 +23,8 @@
  *    Device-detected key-domain errors (identity bucket with key >= m) set
  *    a flag in the workspace that ms_device_status reports; the output of
  *    that call is then unspecified (no out-of-bounds write happens).
- *  - n < 2^32 (offsets are 32-bit).  1 <= m <= 256 (paper scope).
+ *  - n < 2^32 (offsets are 32-bit).  1 <= m <= 256 (paper scope) for
+ *    every call; the multisplit calls also take 256 < m <= 65536 (below).
  */
 #ifndef MULTISPLIT_H_
 #define MULTISPLIT_H_
@@ -49,15 +50,21 @@ typedef enum {
 typedef enum {
   MS_BUCKET_IDENTITY = 0, /* f(u) = u; requires u < m                     */
   MS_BUCKET_DELTA = 1,    /* f(u) = min(floor(u / delta), m-1), delta >= 1 */
-  MS_BUCKET_RADIX = 2     /* f(u) = (u >> shift) & (2^bits - 1), m = 2^bits */
+  MS_BUCKET_RADIX = 2,    /* f(u) = (u >> shift) & (2^bits - 1), m = 2^bits */
+  MS_BUCKET_SPLITTERS = 3 /* f(u) = j with s_j <= u < s_{j+1}: `splitters` holds
+                             the m-1 interior splitters s_1 < ... < s_{m-1} (device memory,
+                             strictly increasing -- not checked; an unordered table gives an
+                             unspecified permutation, never an out-of-bounds write); s_0 = 0
+                             and s_m = 2^32 are the ends of the key domain (R27) */
 } ms_bucket_kind;
 
 typedef struct {
   uint32_t kind;        /* ms_bucket_kind */
-  uint32_t num_buckets; /* m, 1..256 */
+  uint32_t num_buckets; /* m: 1..256, or up to 65536 for the m > 256 path (see below) */
   uint32_t delta;       /* DELTA only: bucket width, >= 1 */
   uint32_t shift;       /* RADIX only: first bit of the digit */
-  uint32_t bits;        /* RADIX only: digit width 1..8, shift + bits <= 32 */
+  uint32_t bits;        /* RADIX only: digit width 1..8 (1..16 when m > 256), shift + bits <= 32 */
+  const uint32_t *splitters; /* SPLITTERS only: m-1 device words (may be NULL when m = 1) */
 } ms_bucket_fn;
 
 /* Human-readable name of a status code (static storage). */
@@ -130,6 +137,15 @@ ms_status ms_bucket_validate(const ms_bucket_fn *fn);
  * exclusive scan of the bucket x tile matrix (Eq.2) -> tile-local stable
  * reorder in shared memory + coalesced scatter.  n <= one tile runs as a
  * single launch.
+ *
+ * m > 256 (Sec.6.3; DELTA / IDENTITY / SPLITTERS up to 65536
+ * buckets, RADIX digits of 9..16 bits): the paper iterates multisplits over at
+ * most 256 buckets; here the iteration is LSD over the 8-bit digits of the
+ * bucket id, which needs no property of f: one pass writes the bucket ids b_i
+ * and payloads (the key, or the index for pairs), two stable radix-digit
+ * multisplits of the (b, payload) pairs sort them by b, the offsets come from
+ * the sorted ids, and pairs are gathered by index.  RADIX digits wider than 8
+ * bits are two radix passes over the keys.  The workspace query covers it.
  * --------------------------------------------------------------------- */
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values);
 

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import MultisplitError, check, ms_bucket_fn
 
-__all__ = ["Bucket", "Delta", "Identity", "Radix", "multisplit", "radix_sort", "device_status",
+__all__ = ["Bucket", "Delta", "Identity", "Radix", "Splitters", "multisplit", "radix_sort", "device_status",
            "prescan", "scan", "tile_size", "radix_pass_schedule", "workspace_size",
            "set_option", "get_option", "device_init", "MultisplitError"]
 
@@ -32,9 +32,11 @@ class Bucket:
     delta: int = 0
     shift: int = 0
     bits: int = 0
+    splitters: torch.Tensor | None = None  # SPLITTERS: m-1 device words
 
     def c(self) -> ms_bucket_fn:
-        return ms_bucket_fn(self.kind, self.m, self.delta, self.shift, self.bits)
+        sp = self.splitters.data_ptr() if self.splitters is not None and self.splitters.numel() else None
+        return ms_bucket_fn(self.kind, self.m, self.delta, self.shift, self.bits, sp)
 
 
 def Delta(m: int, delta: int | None = None) -> Bucket:
@@ -54,6 +56,14 @@ def Identity(m: int) -> Bucket:
 def Radix(shift: int, bits: int) -> Bucket:
     """Radix-digit buckets f(u) = (u >> shift) & (2^bits - 1)."""
     return Bucket(_lib.MS_BUCKET_RADIX, 1 << bits, shift=shift, bits=bits)
+
+
+def Splitters(splitters: torch.Tensor) -> Bucket:
+    """Splitter buckets: the m-1 interior splitters s_1 < ... < s_{m-1} as a CUDA
+    int32/uint32 tensor (bit patterns read as uint32); f(u) = j with s_j <= u < s_{j+1},
+    s_0 = 0 and s_m = 2^32 (reading R27).  The tensor must outlive the calls."""
+    sp = _u32view(splitters, "splitters")
+    return Bucket(_lib.MS_BUCKET_SPLITTERS, sp.numel() + 1, splitters=sp)
 
 
 def _u32view(t: torch.Tensor, name: str, device: torch.device | None = None,

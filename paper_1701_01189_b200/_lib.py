@@ -30,11 +30,13 @@ MS_PIPELINE_TILE = 1
 MS_BUCKET_IDENTITY = 0
 MS_BUCKET_DELTA = 1
 MS_BUCKET_RADIX = 2
+MS_BUCKET_SPLITTERS = 3
 
 
 class ms_bucket_fn(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_uint32), ("num_buckets", ctypes.c_uint32),
-                ("delta", ctypes.c_uint32), ("shift", ctypes.c_uint32), ("bits", ctypes.c_uint32)]
+                ("delta", ctypes.c_uint32), ("shift", ctypes.c_uint32), ("bits", ctypes.c_uint32),
+                ("splitters", ctypes.c_void_p)]
 
 
 # (name, restype, argtypes) for every symbol include/multisplit.h declares.

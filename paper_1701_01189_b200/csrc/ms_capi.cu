@@ -3,6 +3,7 @@
 // radix-sort pass driver.  All launches are stream-ordered; nothing here
 // synchronizes except ms_device_status.
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <mutex>
 #include <cmath>
@@ -159,18 +160,24 @@ Layout layout_for(uint64_t n, uint32_t m, bool pairs, bool ranges = false) {
   return lo;
 }
 
-ms_status validate_fn(const ms_bucket_fn *fn) {
+constexpr uint32_t kMaxLargeM = 65536;  // m > 256: two LSD digit passes of the bucket id
+
+// large: the multisplit entry points also take 256 < m <= 65536 (RADIX digits
+// up to 16 bits); the stage, merge and sharded calls keep the paper's m <= 256
+ms_status validate_fn(const ms_bucket_fn *fn, bool large = false) {
   if (!fn) return MS_ERR_INVALID_VALUE;
   const uint32_t m = fn->num_buckets;
-  if (m < 1 || m > 256) return MS_ERR_UNSUPPORTED;
+  if (m < 1 || m > (large ? kMaxLargeM : 256u)) return MS_ERR_UNSUPPORTED;
   switch (fn->kind) {
     case MS_BUCKET_IDENTITY: return MS_SUCCESS;
     case MS_BUCKET_DELTA: return fn->delta >= 1 ? MS_SUCCESS : MS_ERR_INVALID_VALUE;
     case MS_BUCKET_RADIX:
-      if (fn->bits < 1 || fn->bits > 8) return MS_ERR_INVALID_VALUE;
+      if (fn->bits < 1 || fn->bits > (large ? 16u : 8u)) return MS_ERR_INVALID_VALUE;
       if ((uint64_t)fn->shift + fn->bits > 32) return MS_ERR_INVALID_VALUE;
       if (m != (1u << fn->bits)) return MS_ERR_INVALID_VALUE;
       return MS_SUCCESS;
+    case MS_BUCKET_SPLITTERS:
+      return (m == 1 || fn->splitters) ? MS_SUCCESS : MS_ERR_INVALID_VALUE;
     default: return MS_ERR_INVALID_VALUE;
   }
 }
@@ -188,6 +195,14 @@ Plan make_plan(const ms_bucket_fn *fn) {
   p.m1 = fn->num_buckets - 1;
   switch (fn->kind) {
     case MS_BUCKET_IDENTITY: pl.kind = kIdentity; break;
+    case MS_BUCKET_SPLITTERS: {
+      pl.kind = kSplitters;
+      p.spl = fn->splitters;
+      uint32_t pw = 1;
+      while (pw < p.m) pw <<= 1;
+      p.spl_pow = pw;
+      break;
+    }
     case MS_BUCKET_RADIX:
       pl.kind = fn->shift + fn->bits == 32 ? kTopBits : kRadix;
       p.shift = fn->shift;
@@ -241,80 +256,53 @@ bool overlaps(const void *a, const void *b, uint64_t n) {
   return pa < pb + bytes && pb < pa + bytes;
 }
 
+// Calls f(std::integral_constant<int, K>) with the plan's compile-time bucket kind K.
+template <typename F>
+cudaError_t by_kind(int kind, F &&f) {
+  switch (kind) {
+    case kIdentity: return f(std::integral_constant<int, kIdentity>{});
+    case kDelta: return f(std::integral_constant<int, kDelta>{});
+    case kRadix: return f(std::integral_constant<int, kRadix>{});
+    case kTopBits: return f(std::integral_constant<int, kTopBits>{});
+    case kSplitters: return f(std::integral_constant<int, kSplitters>{});
+    default: return f(std::integral_constant<int, kDeltaShift>{});
+  }
+}
+#define MS_LAUNCH(fn_, ...) \
+  by_kind(pl.kind, [&](auto k_) { return Launch<decltype(k_)::value>::fn_(__VA_ARGS__); })
+
 cudaError_t range_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t per,
                        uint32_t grid, uint32_t *R, uint32_t *hdr, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kDelta: return Launch<kDelta>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kRadix: return Launch<kRadix>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    case kTopBits: return Launch<kTopBits>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-    default: return Launch<kDeltaShift>::range_hist(keys, n, per, grid, pl.bp, R, hdr, s);
-  }
+  return MS_LAUNCH(range_hist, keys, n, per, grid, pl.bp, R, hdr, s);
 }
 
 cudaError_t tile_hist(const Plan &pl, const uint32_t *keys, uint32_t n, uint32_t tile,
                       uint32_t grid, uint32_t *H, uint32_t *hdr, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
-    case kDelta: return Launch<kDelta>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
-    case kRadix: return Launch<kRadix>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
-    case kTopBits: return Launch<kTopBits>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
-    default: return Launch<kDeltaShift>::tile_hist(keys, n, tile, grid, pl.bp, H, hdr, s);
-  }
+  return MS_LAUNCH(tile_hist, keys, n, tile, grid, pl.bp, H, hdr, s);
 }
 
 cudaError_t tile_meta(const Plan &pl, bool pairs, const uint32_t *keys, uint32_t n, uint32_t L,
                       uint32_t K, uint32_t grid, uint32_t *meta, uint32_t *R, uint32_t *hdr,
                       cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
-    case kDelta: return Launch<kDelta>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
-    case kRadix: return Launch<kRadix>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
-    case kTopBits: return Launch<kTopBits>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
-    default: return Launch<kDeltaShift>::tile_meta(pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
-  }
+  return MS_LAUNCH(tile_meta, pairs, keys, n, L, K, grid, pl.bp, meta, R, hdr, s);
 }
 
 cudaError_t fused_meta(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::fused_meta(pairs, a, pl.bp, grid, s);
-    case kDelta: return Launch<kDelta>::fused_meta(pairs, a, pl.bp, grid, s);
-    case kRadix: return Launch<kRadix>::fused_meta(pairs, a, pl.bp, grid, s);
-    case kTopBits: return Launch<kTopBits>::fused_meta(pairs, a, pl.bp, grid, s);
-    default: return Launch<kDeltaShift>::fused_meta(pairs, a, pl.bp, grid, s);
-  }
+  return MS_LAUNCH(fused_meta, pairs, a, pl.bp, grid, s);
 }
 
 cudaError_t tile_meta_wide(const Plan &pl, bool pairs, const uint32_t *keys, uint32_t n, uint32_t LM,
                            uint32_t per, uint32_t grid, uint32_t *meta, uint32_t nkf, uint32_t *R,
                            uint32_t *hdr, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
-    case kDelta: return Launch<kDelta>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
-    case kRadix: return Launch<kRadix>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
-    case kTopBits: return Launch<kTopBits>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
-    default: return Launch<kDeltaShift>::tile_meta_wide(pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
-  }
+  return MS_LAUNCH(tile_meta_wide, pairs, keys, n, LM, per, grid, pl.bp, meta, nkf, R, hdr, s);
 }
 
 cudaError_t fused_meta_wide(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::fused_meta_wide(pairs, a, pl.bp, grid, s);
-    case kDelta: return Launch<kDelta>::fused_meta_wide(pairs, a, pl.bp, grid, s);
-    case kRadix: return Launch<kRadix>::fused_meta_wide(pairs, a, pl.bp, grid, s);
-    case kTopBits: return Launch<kTopBits>::fused_meta_wide(pairs, a, pl.bp, grid, s);
-    default: return Launch<kDeltaShift>::fused_meta_wide(pairs, a, pl.bp, grid, s);
-  }
+  return MS_LAUNCH(fused_meta_wide, pairs, a, pl.bp, grid, s);
 }
 
 cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cudaStream_t s) {
-  switch (pl.kind) {
-    case kIdentity: return Launch<kIdentity>::fused(pairs, a, pl.bp, grid, s);
-    case kDelta: return Launch<kDelta>::fused(pairs, a, pl.bp, grid, s);
-    case kRadix: return Launch<kRadix>::fused(pairs, a, pl.bp, grid, s);
-    case kTopBits: return Launch<kTopBits>::fused(pairs, a, pl.bp, grid, s);
-    default: return Launch<kDeltaShift>::fused(pairs, a, pl.bp, grid, s);
-  }
+  return MS_LAUNCH(fused, pairs, a, pl.bp, grid, s);
 }
 
 // Level-0 pipelines with prescan records: m <= 32 KM -> kf_meta (ms_meta.cuh),
@@ -392,11 +380,106 @@ cudaError_t l0_postscan(const Plan &pl, bool pairs, KfArgs &a, const L0 &st, cud
   return counted(fused_meta_wide(pl, pairs, a, st.G, s));
 }
 
+// ---------------------------------------------------------------- m > 256
+// Sec.6.3: iterated multisplits over <= 256 buckets, here LSD over
+// the 8-bit digits of the bucket id (ms_large.cuh).  RADIX digits wider than 8
+// bits are two radix passes over the keys themselves.
+// Workspace: [hdr][inner multisplit ws][RADIX: keys (+vals) of pass 1 |
+//             else: b0 p0 b1 p1 b2 (+p2 for pairs), n words each]
+struct LargeLayout {
+  size_t inner, inner_bytes, x[6], total;
+};
+LargeLayout large_layout(uint64_t n, uint32_t kind, bool pairs) {
+  LargeLayout lo{};
+  const bool radix = kind == MS_BUCKET_RADIX;
+  lo.inner = kHdrBytes;
+  lo.inner_bytes = ms_multisplit_workspace_size(n, 256, radix ? pairs : true);
+  size_t off = lo.inner + align_up(lo.inner_bytes);
+  const int arrays = radix ? (pairs ? 2 : 1) : (pairs ? 6 : 5);
+  for (int i = 0; i < arrays; ++i) {
+    lo.x[i] = off;
+    off += align_up(n * 4u);
+  }
+  lo.total = off;
+  return lo;
+}
+
+ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                          uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
+                          uint32_t *bucket_offsets, void *ws, size_t ws_bytes, void *stream,
+                          bool pairs);
+
+ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                     uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
+                     uint32_t *bucket_offsets, char *w, cudaStream_t s, bool pairs) {
+  const uint32_t m = fn->num_buckets;
+  const LargeLayout lo = large_layout(n, fn->kind, pairs);
+  void *const *hooks = g_stage_events;
+  g_stage_events = nullptr;  // the inner multisplits record nothing
+  auto ev = [&](int i) {
+    if (hooks) cudaEventRecord((cudaEvent_t)hooks[i], s);
+  };
+  auto done = [&](ms_status st) {
+    g_stage_events = hooks;
+    return st;
+  };
+  char *inner = w + lo.inner;
+  uint32_t *hdr = (uint32_t *)w;
+  ev(0);
+  if (cudaMemsetAsync(hdr, 0, 8, s) != cudaSuccess) return done(MS_ERR_CUDA);
+  if (fn->kind == MS_BUCKET_RADIX) {
+    uint32_t *tk = (uint32_t *)(w + lo.x[0]), *tv = pairs ? (uint32_t *)(w + lo.x[1]) : nullptr;
+    const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, fn->shift, 8u, nullptr};
+    const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (fn->bits - 8u), 0u, fn->shift + 8u, fn->bits - 8u, nullptr};
+    ev(1);
+    ms_status st = multisplit_impl(keys_in, vals_in, tk, tv, n, &a, nullptr, inner, lo.inner_bytes, s, pairs);
+    if (st != MS_SUCCESS) return done(st);
+    ev(2);
+    st = multisplit_impl(tk, tv, keys_out, vals_out, n, &b, nullptr, inner, lo.inner_bytes, s, pairs);
+    if (st != MS_SUCCESS) return done(st);
+    if (bucket_offsets) {
+      k_offsets_sorted<<<min((uint32_t)((n + 256u) / 256u), 148u * 8u), 256, 0, s>>>(
+          keys_out, (uint32_t)n, fn->shift, m - 1u, m, bucket_offsets);
+      if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
+    }
+    ev(3);
+    return done(MS_SUCCESS);
+  }
+  uint32_t *b0 = (uint32_t *)(w + lo.x[0]), *p0 = (uint32_t *)(w + lo.x[1]);
+  uint32_t *b1 = (uint32_t *)(w + lo.x[2]), *p1 = (uint32_t *)(w + lo.x[3]);
+  uint32_t *b2 = (uint32_t *)(w + lo.x[4]);
+  uint32_t *p2 = pairs ? (uint32_t *)(w + lo.x[5]) : keys_out;
+  const Plan pl = make_plan(fn);
+  if (counted(MS_LAUNCH(bucket_ids, keys_in, (uint32_t)n, pl.bp, pairs, b0, p0, hdr, s)) != cudaSuccess)
+    return done(MS_ERR_CUDA);
+  ev(1);
+  uint32_t hb = 0;
+  while ((1u << hb) < m) ++hb;  // bits of the bucket id
+  const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, 0u, 8u, nullptr};
+  const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (hb - 8u), 0u, 8u, hb - 8u, nullptr};
+  ms_status st = multisplit_impl(b0, p0, b1, p1, n, &a, nullptr, inner, lo.inner_bytes, s, true);
+  if (st != MS_SUCCESS) return done(st);
+  ev(2);
+  st = multisplit_impl(b1, p1, b2, p2, n, &b, nullptr, inner, lo.inner_bytes, s, true);
+  if (st != MS_SUCCESS) return done(st);
+  const uint32_t grid = min((uint32_t)((n + 256u) / 256u), 148u * 8u);
+  if (bucket_offsets) {
+    k_offsets_sorted<<<grid, 256, 0, s>>>(b2, (uint32_t)n, 0u, 0xFFFFFFFFu, m, bucket_offsets);
+    if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
+  }
+  if (pairs) {
+    k_gather_pairs<<<grid, 256, 0, s>>>(p2, (uint32_t)n, keys_in, vals_in, keys_out, vals_out);
+    if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
+  }
+  ev(3);
+  return done(MS_SUCCESS);
+}
+
 ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                           uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
                           uint32_t *bucket_offsets, void *ws, size_t ws_bytes, void *stream,
                           bool pairs) {
-  ms_status st = validate_fn(fn);
+  ms_status st = validate_fn(fn, true);
   if (st != MS_SUCCESS) return st;
   if (n >= (1ull << 32)) return MS_ERR_UNSUPPORTED;
   const uint32_t m = fn->num_buckets;
@@ -409,18 +492,20 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
                   overlaps(vals_in, keys_out, n) || overlaps(keys_out, vals_out, n)))
       return MS_ERR_INVALID_VALUE;
   }
-  const Layout lo = layout_for(n, m, pairs);
-  if (ws_bytes < lo.total) return MS_ERR_WORKSPACE;
+  if (ws_bytes < ms_multisplit_workspace_size(n, m, pairs)) return MS_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   char *w = (char *)ws;
   uint32_t *hdr = (uint32_t *)w;
 
   if (n == 0) {
     if (cudaMemsetAsync(hdr, 0, 8, s) != cudaSuccess) return MS_ERR_CUDA;
-    if (bucket_offsets && cudaMemsetAsync(bucket_offsets, 0, (m + 1) * 4u, s) != cudaSuccess)
+    if (bucket_offsets && cudaMemsetAsync(bucket_offsets, 0, ((size_t)m + 1) * 4u, s) != cudaSuccess)
       return MS_ERR_CUDA;
     return MS_SUCCESS;
   }
+  if (m > 256)
+    return large_impl(keys_in, vals_in, keys_out, vals_out, n, fn, bucket_offsets, w, s, pairs);
+  const Layout lo = layout_for(n, m, pairs);
 
   const Plan pl = make_plan(fn);
   KfArgs a{};
@@ -610,31 +695,35 @@ int ms_get_option(int option) {
 
 ms_status ms_bucket_delta_default(uint32_t m, ms_bucket_fn *out) {
   if (!out) return MS_ERR_INVALID_VALUE;
-  if (m < 1 || m > 256) return MS_ERR_UNSUPPORTED;
+  if (m < 1 || m > kMaxLargeM) return MS_ERR_UNSUPPORTED;
   const unsigned long long d = ((1ull << 32) + m - 1) / m;
-  *out = ms_bucket_fn{MS_BUCKET_DELTA, m, (uint32_t)(d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d), 0, 0};
+  *out = ms_bucket_fn{MS_BUCKET_DELTA, m, (uint32_t)(d > 0xFFFFFFFFull ? 0xFFFFFFFFull : d), 0, 0, nullptr};
   return MS_SUCCESS;
 }
 
 ms_status ms_bucket_identity(uint32_t m, ms_bucket_fn *out) {
   if (!out) return MS_ERR_INVALID_VALUE;
-  if (m < 1 || m > 256) return MS_ERR_UNSUPPORTED;
+  if (m < 1 || m > kMaxLargeM) return MS_ERR_UNSUPPORTED;
   *out = ms_bucket_fn{MS_BUCKET_IDENTITY, m, 0, 0, 0};
   return MS_SUCCESS;
 }
 
 ms_status ms_bucket_radix(uint32_t shift, uint32_t bits, ms_bucket_fn *out) {
   if (!out) return MS_ERR_INVALID_VALUE;
-  if (bits < 1 || bits > 8 || (uint64_t)shift + bits > 32) return MS_ERR_INVALID_VALUE;
+  if (bits < 1 || bits > 16 || (uint64_t)shift + bits > 32) return MS_ERR_INVALID_VALUE;
   *out = ms_bucket_fn{MS_BUCKET_RADIX, 1u << bits, 0, shift, bits};
   return MS_SUCCESS;
 }
 
-ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn); }
+ms_status ms_bucket_validate(const ms_bucket_fn *fn) { return validate_fn(fn, true); }
 
 size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
   if (m < 1) m = 1;
-  if (m > 256) m = 256;
+  if (m > 256) {  // the m > 256 path (either identifier layout: the larger one)
+    const size_t a = large_layout(n, MS_BUCKET_DELTA, with_values != 0).total;
+    const size_t b = large_layout(n, MS_BUCKET_RADIX, with_values != 0).total;
+    return a > b ? a : b;
+  }
   return layout_for(n, m, with_values != 0).total;
 }
 
@@ -862,27 +951,8 @@ static ms_status shard_merge(const uint32_t *keys_recv, const uint32_t *vals_rec
   const Plan pl = make_plan(fn);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  switch (pl.kind) {
-    case kIdentity:
-      e = Launch<kIdentity>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
-                                   recv_starts, merge_offsets, G, keys_out, vals_out, s);
-      break;
-    case kDelta:
-      e = Launch<kDelta>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp, recv_starts,
-                                merge_offsets, G, keys_out, vals_out, s);
-      break;
-    case kRadix:
-      e = Launch<kRadix>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp, recv_starts,
-                                merge_offsets, G, keys_out, vals_out, s);
-      break;
-    case kTopBits:
-      e = Launch<kTopBits>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
-                                  recv_starts, merge_offsets, G, keys_out, vals_out, s);
-      break;
-    default:
-      e = Launch<kDeltaShift>::merge(pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp,
-                                     recv_starts, merge_offsets, G, keys_out, vals_out, s);
-  }
+  e = MS_LAUNCH(merge, pairs, keys_recv, vals_recv, (uint32_t)n_recv, pl.bp, recv_starts,
+                merge_offsets, G, keys_out, vals_out, s);
   return counted(e) == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
 }
 

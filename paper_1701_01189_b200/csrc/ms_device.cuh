@@ -27,7 +27,8 @@ enum BucketKind : uint32_t {
   kDelta = 1,
   kRadix = 2,
   kDeltaShift = 3,
-  kTopBits = 4
+  kTopBits = 4,
+  kSplitters = 5
 };
 
 // Bucket identifier parameters, precomputed on the host.
@@ -39,7 +40,36 @@ struct BucketParams {
   uint32_t magic_hi; // DELTA: M = ceil(2^64 / delta) split in two words
   uint32_t magic_lo;
   uint32_t delta_is_one;
+  uint32_t spl_pow;          // SPLITTERS: smallest power of two >= m
+  const uint32_t *spl;       // SPLITTERS: the m-1 interior splitters s_1 < ... < s_{m-1}
+                             // (global on entry; kernels re-point it at a shared copy)
 };
+
+// SPLITTERS (reading R27): f(u) = the j with s_j <= u <
+// s_{j+1}, s_0 = 0 and s_m = 2^32 the ends of the key domain, i.e. the number
+// of interior splitters <= u.  Branch-free upper-bound search with
+// power-of-two steps (log2 spl_pow probes of the table).
+__device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketParams &p) {
+  uint32_t j = 0;
+#pragma unroll 1
+  for (uint32_t step = p.spl_pow >> 1; step != 0; step >>= 1) {
+    const uint32_t t = j + step;  // are the first t splitters all <= u?
+    if (t <= p.m1 && p.spl[t - 1] <= u) j = t;
+  }
+  return j;
+}
+
+// Every kernel templated on the bucket kind starts with this: for SPLITTERS it
+// copies the table into shared memory (CAP >= m-1 entries) and re-points
+// bp.spl at the copy, so that the per-key search probes shared memory.
+#define MS_STAGE_SPLITTERS(bp_, CAP)                                            \
+  if constexpr (KIND == kSplitters) {                                           \
+    __shared__ uint32_t ms_s_spl[CAP];                                          \
+    for (uint32_t i_ = threadIdx.x; i_ < (bp_).m1 && i_ < (CAP); i_ += blockDim.x) \
+      ms_s_spl[i_] = __ldg((bp_).spl + i_);                                     \
+    __syncthreads();                                                            \
+    (bp_).spl = ms_s_spl;                                                       \
+  }
 
 // f(u) for the three identifiers.  DELTA computes
 // floor(u / delta) exactly as the high 64 bits of u * ceil(2^64/delta): the
@@ -57,6 +87,8 @@ __device__ __forceinline__ uint32_t bucket_of(uint32_t u, const BucketParams &p)
     return q < p.m1 ? q : p.m1;
   } else if constexpr (KIND == kIdentity) {
     return u < p.m1 ? u : p.m1;
+  } else if constexpr (KIND == kSplitters) {
+    return splitter_bucket(u, p);
   } else {
     uint32_t q;
     if (p.delta_is_one) {

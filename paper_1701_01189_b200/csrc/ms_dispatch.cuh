@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "ms_wide.cuh"
+#include "ms_large.cuh"
 
 #include <atomic>
 
@@ -50,6 +51,14 @@ struct Launch {
                                     cudaStream_t s);
   static cudaError_t fused_meta_wide(bool pairs, const KfArgs &a, const BucketParams &bp,
                                      uint32_t grid, cudaStream_t s);
+  // m > 256 (ms_large.cuh): bucket ids and payloads of every key
+  static cudaError_t bucket_ids(const uint32_t *keys, uint32_t n, const BucketParams &bp,
+                                bool payload_index, uint32_t *b, uint32_t *p, uint32_t *hdr,
+                                cudaStream_t s) {
+    const uint32_t grid = min((n + 255u) / 256u, 148u * 8u);
+    k_bucket_ids<KIND><<<grid ? grid : 1u, 256, 0, s>>>(keys, n, bp, payload_index ? 1 : 0, b, p, hdr);
+    return cudaGetLastError();
+  }
   static cudaError_t merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
                            const BucketParams &bp, const uint32_t *starts, const uint32_t *offs,
                            uint32_t G, uint32_t *keys_out, uint32_t *vals_out, cudaStream_t s);

@@ -175,6 +175,7 @@ template <int KIND, bool SMALLM>
 __global__ void __launch_bounds__(kThreads)
     ku_range_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t elems_per_cta,
                   BucketParams bp, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   extern __shared__ uint32_t ku_smem[];  // [kWarps][m]
   __shared__ uint32_t s_red[kWarps];
   griddep_launch_dependents();  // let KR (programmatic launch) get scheduled early
@@ -199,6 +200,7 @@ template <int KIND, bool SMALLM>
 __global__ void __launch_bounds__(kThreads)
     kh_tile_hist(const uint32_t *__restrict__ keys, uint32_t n, uint32_t tile, BucketParams bp,
                  uint32_t *__restrict__ H, uint32_t *__restrict__ hdr) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   extern __shared__ uint32_t kh_smem[];
   __shared__ uint32_t s_red[kWarps];
   const uint32_t m = bp.m, tid = threadIdx.x;
@@ -685,6 +687,7 @@ __device__ __forceinline__ void kf_do_tile(const KfArgs &a, const BucketParams &
 
 template <int KIND, bool PAIRS, bool SMALLM, int W, int ITEMS, int MINB, int SCAN>
 __global__ void __launch_bounds__(W * 32, MINB) kf_fused(KfArgs a, BucketParams bp) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   constexpr bool WSCAN = SCAN != 0;
   constexpr uint32_t NT = W * 32;
   constexpr uint32_t T = NT * ITEMS;
@@ -831,6 +834,7 @@ __global__ void __launch_bounds__(256)
                    uint32_t n, BucketParams bp, const uint32_t *__restrict__ starts,
                    const uint32_t *__restrict__ offs, uint32_t G, uint32_t *__restrict__ keys_out,
                    uint32_t *__restrict__ vals_out) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     uint32_t s = 0;
     while (s + 1 < G && __ldg(starts + s + 1) <= e) ++s;

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
     km_tile_meta(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
                  uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  MS_STAGE_SPLITTERS(bp, 32);
   constexpr uint32_t W = kWarps;
   constexpr uint32_t SL = 32u * ITEMS;  // keys per warp slice
   constexpr uint32_t T = W * SL;
@@ -289,6 +290,7 @@ enum : int { kRankBallot = 0, kRankVote2 = 2, kRankMasks = 7, kRankInc = 8 };
 // ============================================================================
 template <int KIND, bool PAIRS, bool SMALLM, int ITEMS, int RANK, bool PROD>
 __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(KfArgs a, BucketParams bp) {
+  MS_STAGE_SPLITTERS(bp, 32);
   constexpr uint32_t W = kWarps, NT = kThreads;  // consumer warps / threads
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t kStages = 3;

@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
     km_meta_wide(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
                  uint32_t num_kf_tiles, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   constexpr uint32_t W = kWarps, SL = 512, T = kWideKmTile, KS = kmw_stages(NB);
   constexpr uint32_t HW = NB / 2;                 // packed record words per lane per row
   constexpr uint32_t RW = 16u * NB;               // packed record words per row (mP / 2)
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 // ============================================================================
 template <int KIND, bool PAIRS, int NB>
 __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a, BucketParams bp) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   constexpr uint32_t W = wide_kw(PAIRS), NT = W * 32, ITEMS = 16;
   constexpr uint32_t T = NT * ITEMS;
   constexpr uint32_t kStages = 3, kPrefetch = 2;

@@ -65,7 +65,15 @@ def test_bucket_helpers(lib):
         assert fn.kind == _lib.MS_BUCKET_DELTA and fn.num_buckets == m
         assert fn.delta == min(-(-(1 << 32) // m), (1 << 32) - 1)
     assert lib.ms_bucket_delta_default(0, ctypes.byref(fn)) == _lib.MS_ERR_UNSUPPORTED
-    assert lib.ms_bucket_delta_default(257, ctypes.byref(fn)) == _lib.MS_ERR_UNSUPPORTED
+    # m > 256 (Sec.6.3): up to 65536 buckets through the multisplit entry points
+    assert lib.ms_bucket_delta_default(257, ctypes.byref(fn)) == 0 and fn.delta == -(-(1 << 32) // 257)
+    assert lib.ms_bucket_delta_default(65537, ctypes.byref(fn)) == _lib.MS_ERR_UNSUPPORTED
+    assert lib.ms_bucket_radix(8, 16, ctypes.byref(fn)) == 0 and fn.num_buckets == 65536
+    assert lib.ms_bucket_radix(0, 17, ctypes.byref(fn)) == _lib.MS_ERR_INVALID_VALUE
+    spl = _lib.ms_bucket_fn(_lib.MS_BUCKET_SPLITTERS, 4, 0, 0, 0, None)
+    assert lib.ms_bucket_validate(ctypes.byref(spl)) == _lib.MS_ERR_INVALID_VALUE  # no table
+    one = _lib.ms_bucket_fn(_lib.MS_BUCKET_SPLITTERS, 1, 0, 0, 0, None)
+    assert lib.ms_bucket_validate(ctypes.byref(one)) == 0
     assert lib.ms_bucket_radix(24, 8, ctypes.byref(fn)) == 0 and fn.num_buckets == 256
     assert lib.ms_bucket_radix(25, 8, ctypes.byref(fn)) == _lib.MS_ERR_INVALID_VALUE
     assert lib.ms_bucket_radix(0, 0, ctypes.byref(fn)) == _lib.MS_ERR_INVALID_VALUE

@@ -87,7 +87,9 @@ def test_identity_domain_and_validation():
         oracle.multisplit([0, 1, 9], oracle.identity(8))
     assert oracle.validate(oracle.Bucket(oracle.DELTA, 4, delta=0)) == oracle.ERR_INVALID
     assert oracle.validate(oracle.Bucket(oracle.IDENTITY, 0)) == oracle.ERR_UNSUPPORTED
-    assert oracle.validate(oracle.Bucket(oracle.IDENTITY, 257)) == oracle.ERR_UNSUPPORTED
+    # m > 256 is the extended regime of Sec.6.3, up to 65536 buckets
+    assert oracle.validate(oracle.Bucket(oracle.IDENTITY, 257)) == oracle.OK
+    assert oracle.validate(oracle.Bucket(oracle.IDENTITY, 65537)) == oracle.ERR_UNSUPPORTED
     assert oracle.validate(oracle.Bucket(oracle.RADIX, 256, shift=25, bits=8)) == oracle.ERR_INVALID
     assert oracle.validate(oracle.Bucket(oracle.RADIX, 128, shift=0, bits=8)) == oracle.ERR_INVALID
     assert oracle.validate(oracle.radix(24, 8)) == oracle.OK
