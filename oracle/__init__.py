@@ -68,7 +68,8 @@ def _load():
         lib.orc_validate_ex.argtypes = [u32, u32, u64, u32, u32, p]
         lib.orc_bucket_ex.argtypes = [u32, u32, u64, u32, u32, p, u32, ctypes.POINTER(u32)]
         lib.orc_multisplit_ex.argtypes = [p, p, p, p, u64, u32, u32, u64, u32, u32, p, p]
-        for f in (lib.orc_validate_ex, lib.orc_bucket_ex, lib.orc_multisplit_ex):
+        lib.orc_sssp.argtypes = [p, p, p, u32, u32, p]
+        for f in (lib.orc_validate_ex, lib.orc_bucket_ex, lib.orc_multisplit_ex, lib.orc_sssp):
             f.restype = ctypes.c_int
         for f in (lib.orc_validate, lib.orc_bucket, lib.orc_multisplit,
                   lib.orc_tile_histogram, lib.orc_radix_sort, lib.orc_histogram_even,
@@ -227,3 +228,14 @@ def histogram_range(samples, splitters) -> np.ndarray:
     if st:
         raise OracleError(st)
     return c
+
+
+def sssp(row_ptr, col, w, source: int) -> np.ndarray:
+    """Shortest distances from `source` (Sec.7.2, Dijkstra); 0xFFFFFFFF = unreachable."""
+    row_ptr, col, w = _u32(row_ptr), _u32(col), _u32(w)
+    V = row_ptr.size - 1
+    dist = np.empty(max(V, 1), np.uint32)
+    st = _load().orc_sssp(_ptr(row_ptr), _ptr(col), _ptr(w), V, source, _ptr(dist))
+    if st:
+        raise OracleError(st)
+    return dist[:V]

@@ -50,6 +50,14 @@
  *                       j with s_j <= x < s_{j+1}, found by the upper-bound
  *                       search the paper names, written here as a linear
  *                       count of splitters <= x (reading R26).
+ *   orc_sssp            single-source shortest paths (Sec.7.2):
+ *                       the minimum-cost path from the source to every
+ *                       vertex, computed by Dijkstra's algorithm (P:1805,
+ *                       a single priority queue, vertices settled from the
+ *                       lowest to the highest distance) with a textbook binary
+ *                       heap and lazy deletion; distances of unreachable
+ *                       vertices are 0xFFFFFFFF; a reachable distance >=
+ *                       2^32-1 is not representable (ORC_ERR_UNSUPPORTED).
  *   orc_radix_sort      the result of multisplit-sort (Sec.7.1):
  *                       a stable sort of (keys,values) by the key bits
  *                       [begin_bit, end_bit) as unsigned integers, written as
@@ -337,4 +345,70 @@ int orc_histogram_range(const float *x, uint64_t n, uint32_t m, const float *s,
     counts[le - 1]++;
   }
   return ORC_OK;
+}
+
+/* ------------------------------------------------------------------- SSSP
+ * Sec.7.2.  CSR graph: row_ptr[V+1], col[E], w[E] (weights >= 0).
+ * dist[V] receives the shortest distances from `source`. */
+typedef struct { uint64_t d; uint32_t v; } orc_heap_item;
+
+static void orc_heap_push(orc_heap_item *h, uint64_t *size, orc_heap_item x) {
+  uint64_t i = (*size)++;
+  h[i] = x;
+  while (i > 0) {                          /* sift up */
+    uint64_t p = (i - 1) / 2;
+    if (h[p].d <= h[i].d) break;
+    orc_heap_item t = h[p]; h[p] = h[i]; h[i] = t;
+    i = p;
+  }
+}
+
+static orc_heap_item orc_heap_pop(orc_heap_item *h, uint64_t *size) {
+  orc_heap_item top = h[0];
+  h[0] = h[--(*size)];
+  uint64_t i = 0;
+  for (;;) {                               /* sift down */
+    uint64_t l = 2 * i + 1, r = l + 1, s = i;
+    if (l < *size && h[l].d < h[s].d) s = l;
+    if (r < *size && h[r].d < h[s].d) s = r;
+    if (s == i) break;
+    orc_heap_item t = h[s]; h[s] = h[i]; h[i] = t;
+    i = s;
+  }
+  return top;
+}
+
+int orc_sssp(const uint32_t *row_ptr, const uint32_t *col, const uint32_t *w, uint32_t V,
+             uint32_t source, uint32_t *dist) {
+  if (V == 0 || source >= V) return ORC_ERR_INVALID;
+  const uint64_t E = row_ptr[V];
+  uint64_t *d = (uint64_t *)malloc((size_t)V * sizeof(uint64_t));
+  unsigned char *done = (unsigned char *)calloc(V, 1);
+  orc_heap_item *h = (orc_heap_item *)malloc((size_t)(E + 1) * sizeof(orc_heap_item));
+  if (!d || !done || !h) { free(d); free(done); free(h); return ORC_ERR_INVALID; }
+  for (uint32_t v = 0; v < V; ++v) d[v] = UINT64_MAX;
+  uint64_t size = 0;
+  d[source] = 0;
+  orc_heap_push(h, &size, (orc_heap_item){0, source});
+  while (size > 0) {
+    orc_heap_item it = orc_heap_pop(h, &size);
+    if (done[it.v] || it.d != d[it.v]) continue;   /* a stale queue entry */
+    done[it.v] = 1;                                /* settled: lowest distance first */
+    for (uint64_t e = row_ptr[it.v]; e < row_ptr[it.v + 1]; ++e) {
+      const uint32_t u = col[e];
+      const uint64_t nd = it.d + w[e];
+      if (nd < d[u]) {                             /* relaxation */
+        d[u] = nd;
+        orc_heap_push(h, &size, (orc_heap_item){nd, u});
+      }
+    }
+  }
+  int st = ORC_OK;
+  for (uint32_t v = 0; v < V; ++v) {
+    if (d[v] == UINT64_MAX) dist[v] = 0xFFFFFFFFu;
+    else if (d[v] >= 0xFFFFFFFFull) st = ORC_ERR_UNSUPPORTED;
+    else dist[v] = (uint32_t)d[v];
+  }
+  free(d); free(done); free(h);
+  return st;
 }
