@@ -76,12 +76,39 @@ WORKLOADS = {
                       desc="device-wide Even histogram, 2^25 floats U[0,1024) (Sec.7.3, f2)"),
     "hist_range": dict(n=1 << 25, pairs=False, kind="hist_range", m=256, unit="Gsamples/s", bpe=4,
                        desc="device-wide Range histogram, 2^25 floats U[0,1024), m-1 random splitters (f2)"),
+    # Multisplit-SSSP (Sec.7.2, f4): R-MAT scale 20 (1 M vertices), 5 edges per vertex made
+    # undirected (10.5 M arcs, average degree 10; the paper's rmat: 0.8 M vertices, average
+    # degree 12); weights 0..1000; source 0; delta 100, 10 buckets
+    "sssp_rmat": dict(n=0, pairs=False, kind="sssp", m=10, unit="MTEPS", bpe=0, scale=20, ef=5,
+                      delta=100, desc="Multisplit-SSSP on an undirected R-MAT graph, scale 20, "
+                                      "edge factor 5, weights 0..1000 (Sec.7.2, f4)"),
+    # splitter buckets (f3): m-1 random sorted splitters over uniform keys
+    "ms_keys_spl": dict(n=1 << 25, pairs=False, kind="splitters", m=32, unit="Gkeys/s", bpe=12,
+                        desc="key-only multisplit, n=2^25 uniform uint32, m-1 random splitters (f3)"),
+    "ms_pairs_spl": dict(n=1 << 25, pairs=True, kind="splitters", m=256, unit="Gpairs/s", bpe=20,
+                         desc="key-value multisplit, n=2^25 uniform uint32, m-1 random splitters (f3)"),
+    # m > 256 (f3, Sec.6.3): delta buckets, LSD over the bucket id's 8-bit digits
+    "ms_keys_large": dict(n=1 << 25, pairs=False, kind="delta", m=4096, unit="Gkeys/s", bpe=12,
+                          desc="key-only multisplit, n=2^25 uniform uint32, m > 256 delta buckets (f3)"),
+    "ms_pairs_large": dict(n=1 << 25, pairs=True, kind="delta", m=4096, unit="Gpairs/s", bpe=20,
+                           desc="key-value multisplit, n=2^25 uniform uint32, m > 256 delta buckets (f3)"),
     "sort_keys_r4": dict(n=1 << 28, pairs=False, kind="sort", m=16, bits=4, unit="Gkeys/s", bpe=96,
                          desc="multisplit LSD radix sort, 2^28 uint32 keys, 8 x 4-bit"),
     "sort_pairs_r4": dict(n=1 << 28, pairs=True, kind="sort", m=16, bits=4, unit="Gpairs/s", bpe=160,
                           desc="multisplit LSD radix sort, 2^28 pairs, 8 x 4-bit"),
 }
 SEED = 0x5EED
+
+
+def metric_name(wl, name, m):
+    k = wl["kind"]
+    if k == "sort":
+        return f"radix sort {wl['unit']} ({name})"
+    if k == "sssp":
+        return f"Multisplit-SSSP {wl['unit']} ({name}, K={m} buckets)"
+    if k.startswith("hist"):
+        return f"histogram {wl['unit']} ({name}, m={m})"
+    return f"multisplit {wl['unit']} ({name}, m={m})"
 
 
 def load_peaks():
@@ -182,6 +209,23 @@ class Runner:
             bits = m.bit_length() - 1
             self.bucket = ms.Radix(0, bits)
             gdev.keys_(self.keys, SEED + rank, kind=gen.RADIX, m=m, shift=0, bits=bits, dist=dist, alpha=0.1)
+        elif kind == "splitters":
+            import numpy as np
+            r = np.random.default_rng(SEED + m)
+            spl = np.sort(r.choice(1 << 32, size=m - 1, replace=False).astype(np.uint64)).astype(np.uint32)
+            self.spl = torch.from_numpy(spl.view(np.int32)).to(dev)
+            self.bucket = ms.Splitters(self.spl)
+            gdev.keys_(self.keys, SEED + rank)
+        elif kind == "sssp":
+            from gen.graphs import rmat_csr
+            import numpy as np
+            self.bucket = None
+            V, rp, col, w = rmat_csr(wl["scale"], wl["ef"], SEED, undirected=True)
+            self.graph_host = (rp, col, w)
+            cv = lambda a: torch.from_numpy(a.view(np.int32)).to(dev)  # noqa: E731
+            self.rp, self.col, self.w = cv(rp), cv(col), cv(w)
+            self.dist = torch.empty(V, dtype=torch.int32, device=dev)
+            n = self.n = int(col.size)  # arcs: the MTEPS numerator
         elif kind.startswith("hist"):
             import numpy as np
             self.bucket = None
@@ -198,7 +242,10 @@ class Runner:
         self.ko = torch.empty_like(self.keys)
         self.vo = torch.empty_like(self.vals) if self.vals is not None else None
         self.off = torch.empty(m + 1, dtype=torch.int32, device=dev)
-        if kind == "sort":
+        if kind == "sssp":
+            self.ws = torch.empty(ms._lib.load().ms_sssp_workspace_size(self.rp.numel() - 1, n, m),
+                                  dtype=torch.uint8, device=dev)
+        elif kind == "sort":
             self.ws = torch.empty(ms.radix_sort_workspace_size(n, wl["pairs"]), dtype=torch.uint8, device=dev)
         elif world > 1:
             from paper_1701_01189_b200 import sharded
@@ -210,6 +257,11 @@ class Runner:
             self.ws = torch.empty(max(1, ms.workspace_size(n, m, wl["pairs"])), dtype=torch.uint8, device=dev)
         ms.device_init(dev.index)
 
+    def sssp_stats(self):
+        _, st = self.ms.sssp(self.rp, self.col, self.w, 0, delta=self.wl["delta"], buckets=self.m,
+                             out=self.dist, workspace=self.ws, stats=True)
+        return st
+
     def step(self, keys=None, ko=None):
         keys = self.keys if keys is None else keys
         ko = self.ko if ko is None else ko
@@ -217,6 +269,10 @@ class Runner:
             from paper_1701_01189_b200 import sharded
             sharded.multisplit(self.comm, keys, self.vals, bucket=self.bucket, out_keys=ko,
                                out_values=self.vo, workspace=self.ws)
+            return
+        if self.wl["kind"] == "sssp":
+            self.ms.sssp(self.rp, self.col, self.w, 0, delta=self.wl["delta"], buckets=self.m,
+                         out=self.dist, workspace=self.ws)
             return
         if self.wl["kind"] == "hist_even":
             self.ms.histogram_even(self.samples, self.m, 0.0, 1024.0, out=self.counts)
@@ -275,6 +331,28 @@ def e2e_steps(run: Runner, steps: int, warmup: int):
     multisplit / sort, D2H of the outputs (and offsets), all inside the timed region."""
     import torch
     n = run.n
+    if run.wl["kind"] == "sssp":  # H2D of the CSR graph, D2H of the distances
+        hosts = [torch.from_numpy(a.view("int32")).pin_memory() for a in run.graph_host]
+        devs = [torch.empty_like(x, device=run.rp.device) for x in hosts]
+        dh = torch.empty(run.dist.numel(), dtype=torch.int32).pin_memory()
+
+        def one_s():
+            for d_, h_ in zip(devs, hosts):
+                d_.copy_(h_, non_blocking=True)
+            run.ms.sssp(devs[0], devs[1], devs[2], 0, delta=run.wl["delta"], buckets=run.m, out=run.dist,
+                        workspace=run.ws)
+            dh.copy_(run.dist, non_blocking=True)
+
+        for _ in range(max(1, warmup)):
+            one_s()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            one_s()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / steps, sum(4 * h.numel() for h in hosts), 4 * dh.numel()
     if run.wl["kind"].startswith("hist"):  # H2D of the samples, D2H of the m counts
         xh = run.samples.cpu().pin_memory()
         ch = torch.empty(run.m, dtype=torch.int32).pin_memory()
@@ -371,7 +449,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     n = run.n
-    value = n * world / (ms_step * 1e-3) / 1e9  # all ranks' elements / max-over-ranks step time
+    uscale = 1e6 if wl["unit"] == "MTEPS" else 1e9
+    value = n * world / (ms_step * 1e-3) / uscale  # all ranks' elements / max-over-ranks step time
     # dominant kernel = KF (kf_fused); algorithmic bytes per launch: read + write of keys (+ values)
     roofline = None
     if wl["kind"].startswith("hist"):  # one kernel (kh_histogram) + a counts memset
@@ -389,13 +468,11 @@ def run_ours(args, rank, world, local_rank):
                     "traffic": load_traffic(f"{args.workload}_m{m}"),
                     "alg_bytes_per_launch": ks_bytes, "peak_source": peak_src,
                     "stage_ms": {k: round(v, 5) for k, v in stages.items()}}
-    whole_frac = value * 1e9 / world * wl["bpe"] / (hbm * 1e9)
-    nominal_frac = value * 1e9 / world * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9)
+    whole_frac = value * uscale / world * wl["bpe"] / (hbm * 1e9)
+    nominal_frac = value * uscale / world * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9)
     e2e_ms, h2d, d2h = e2e_steps(run, max(3, args.steps // 4), 2)
     out = {
-        "metric": (f"histogram {wl['unit']} ({args.workload}, m={m})" if wl["kind"].startswith("hist") else
-                   f"multisplit {wl['unit']} ({args.workload}, m={m})") if wl["kind"] != "sort"
-        else f"radix sort {wl['unit']} ({args.workload})",
+        "metric": metric_name(wl, args.workload, m),
         "value": round(value, 3), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
         "scaling": "strong" if wl.get("strong") else "weak", "vs_baseline": None, "dtype": "f32" if wl["kind"].startswith("hist") else "u32",
@@ -407,7 +484,7 @@ def run_ours(args, rank, world, local_rank):
         "hbm_roofline_frac_whole_op": round(whole_frac, 4),
         "hbm_roofline_frac_whole_op_nominal_8tbs": round(nominal_frac, 4),
         "roofline": roofline,
-        "e2e": {"value": round(n * world / (e2e_ms * 1e-3) / 1e9, 3), "unit": wl["unit"],
+        "e2e": {"value": round(n * world / (e2e_ms * 1e-3) / uscale, 3), "unit": wl["unit"],
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -435,7 +512,10 @@ def sweep(args, dev, flush, hbm):
              ("ms_pairs_c3_radix", 64), ("ms_pairs_c3_radix", 128), ("ms_pairs_c3_radix", 256),
              ("ms_pairs_c3_radix_skew", 256),
              ("sort_keys", 256), ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32),
-             ("hist_even", 2), ("hist_even", 256), ("hist_range", 2), ("hist_range", 256)]
+             ("hist_even", 2), ("hist_even", 256), ("hist_range", 2), ("hist_range", 256),
+             ("ms_keys_spl", 32), ("ms_keys_spl", 256), ("ms_pairs_spl", 256),
+             ("ms_keys_large", 1024), ("ms_keys_large", 65536), ("ms_pairs_large", 4096),
+             ("sssp_rmat", 10)]
     for name, m in cases:
         wl = WORKLOADS[name]
         run = Runner(wl, m, dev)
@@ -443,10 +523,13 @@ def sweep(args, dev, flush, hbm):
         times, _, _ = time_steps(run, steps, 3, flush, stage_events=False)
         _, stages, _ = time_steps(run, 3, 1, flush, stage_events=True)
         t = sum(times) / len(times)
-        rate = wl["n"] / (t * 1e-3) / 1e9
+        us = 1e6 if wl["unit"] == "MTEPS" else 1e9
+        rate = run.n / (t * 1e-3) / us
         e = {"value": round(rate, 2), "unit": wl["unit"], "ms": round(t, 4),
-             "hbm_frac": round(rate * 1e9 * wl["bpe"] / (hbm * 1e9), 3),
-             "hbm_frac_nominal": round(rate * 1e9 * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9), 3)}
+             "hbm_frac": round(rate * us * wl["bpe"] / (hbm * 1e9), 3),
+             "hbm_frac_nominal": round(rate * us * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9), 3)}
+        if wl["kind"] == "sssp":
+            e["iterations"] = run.sssp_stats()["iterations"]
         if stages:
             e["stage_ms"] = {k: round(v, 4) for k, v in stages.items()}
             e["kf_frac"] = round(wl["n"] * (16 if wl["pairs"] else 8) / (stages["postscan"] * 1e-3) / 1e9 / hbm, 3)
@@ -526,6 +609,16 @@ def _oracle_sample(wl, m, n_sample):
     elif kind == "identity":
         fn = oracle.identity(m)
         k = gen.keys(n_sample, SEED, kind=gen.IDENTITY, m=m, dist=dist, alpha=0.1)
+    elif kind == "splitters":
+        r = np.random.default_rng(SEED + m)
+        fn = oracle.splitters(np.sort(r.choice(1 << 32, size=m - 1, replace=False).astype(np.uint64)))
+        k = gen.keys(n_sample, SEED)
+    elif kind == "sssp":  # the R-MAT graph at the workload's scale, or 2 smaller for a bounded sample
+        from gen.graphs import rmat_csr
+        V, rp, col, w = rmat_csr(wl["scale"] - (2 if n_sample < (1 << 25) else 0), wl["ef"], SEED, undirected=True)
+        f = lambda: oracle.sssp(rp, col, w, 0)  # noqa: E731
+        f.units = int(col.size)
+        return f
     else:
         fn = None
         k = gen.keys(n_sample, SEED)
@@ -544,15 +637,17 @@ def _oracle_sample(wl, m, n_sample):
 
 def cpu_baseline(wl, m, budget_s: float = 12.0):
     """The oracle as it stands (single-threaded C) on the host, bounded sample."""
-    n_sample = min(wl["n"], 1 << 25) if wl["kind"] != "sort" else (1 << 22)
+    n_sample = min(wl["n"], 1 << 25) if wl["kind"] not in ("sort", "sssp") else (1 << 22 if wl["kind"] == "sort" else 1 << 25)
     f = _oracle_sample(wl, m, n_sample)
+    n_sample = getattr(f, "units", n_sample)
+    us = 1e6 if wl["unit"] == "MTEPS" else 1e9
     f()
     reps, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < budget_s:
         f()
         reps += 1
     dt = (time.perf_counter() - t0) / reps
-    return {"value": round(n_sample / dt / 1e9, 4), "unit": wl["unit"], "cores": 1, "kind": "oracle",
+    return {"value": round(n_sample / dt / us, 4), "unit": wl["unit"], "cores": 1, "kind": "oracle",
             "sample": f"{reps} x {n_sample} elements of the same workload (seed {SEED})",
             "host_cores_available": len(os.sched_getaffinity(0))}
 
@@ -567,7 +662,7 @@ def cpu_parallel(wl, m, budget_s: float = 6.0):
     cores = len(os.sched_getaffinity(0))
     kind = wl["kind"]
     n_sample = min(wl["n"], 1 << 25)
-    if kind.startswith("hist"):
+    if kind.startswith("hist") or kind in ("sssp", "splitters") or m > 256:
         return None
     if kind == "sort":
         k = gen.keys(n_sample, SEED)
@@ -601,6 +696,7 @@ def run_reference(args, rank, world):
     m = args.m or wl["m"]
     n_sample = min(wl["n"], 1 << 24) if wl["kind"] != "sort" else (1 << 21)
     f = _oracle_sample(wl, m, n_sample)
+    n_sample = getattr(f, "units", n_sample)
     for _ in range(args.warmup):
         f()
     ts = []
@@ -609,11 +705,9 @@ def run_reference(args, rank, world):
         f()
         ts.append(time.perf_counter() - t0)
     dt = sum(ts) / len(ts)
-    value = n_sample / dt / 1e9
+    value = n_sample / dt / (1e6 if wl["unit"] == "MTEPS" else 1e9)
     out = {"impl": "reference",
-           "metric": (f"histogram {wl['unit']} ({args.workload}, m={m})" if wl["kind"].startswith("hist") else
-                   f"multisplit {wl['unit']} ({args.workload}, m={m})") if wl["kind"] != "sort"
-           else f"radix sort {wl['unit']} ({args.workload})",
+           "metric": metric_name(wl, args.workload, m),
            "value": round(value, 4), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if wl["kind"].startswith("hist") else "u32", "data": "synthetic (seeded counter-based generator)",

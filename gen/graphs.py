@@ -41,6 +41,11 @@ def to_csr(V: int, src, dst, w):
     return row_ptr, dst[order].astype(np.uint32), w[order].astype(np.uint32)
 
 
-def rmat_csr(scale: int, edge_factor: int, seed: int):
+def rmat_csr(scale: int, edge_factor: int, seed: int, undirected: bool = False):
+    """R-MAT CSR; undirected=True adds the reverse arc of every edge (same weight), the
+    paper's rmat (Table graphs: 0.8 M vertices, 4.8 M edges, average degree 12 = 2 x 4.8 / 0.8,
+    and its MTEPS = 9.6 M arcs / time; reading R29)."""
     V, s, d, w = rmat_edges(scale, edge_factor, seed)
+    if undirected:
+        s, d, w = np.concatenate([s, d]), np.concatenate([d, s]), np.concatenate([w, w])
     return (V,) + to_csr(V, s, d, w)

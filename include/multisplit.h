@@ -358,6 +358,40 @@ ms_status ms_shard_scatter(const uint32_t *keys_in, const uint32_t *vals_in, uin
                            uint64_t *global_bucket_offsets, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Multisplit-SSSP (Sec.7.2): single-source shortest paths by
+ * delta-stepping with the Bucketing strategy, the bucketing
+ * step being ms_multisplit_pairs with splitter buckets.  Each
+ * iteration splits the work list (key = tentative distance, value = vertex)
+ * into K buckets of width `delta` starting at the smallest tentative distance
+ * (the last bucket takes everything beyond), relaxes the out-edges of bucket
+ * 0's up-to-date items (atomicMin on dist) and appends every improvement to
+ * the carried-over buckets 1..K-1.  The loop ends when the work list is empty.
+ *
+ *   row_ptr (V+1), col (E), w (E)   CSR graph in device memory, weights >= 0;
+ *                                   E < 2^32; parallel edges and self loops
+ *                                   are allowed.
+ *   source < V, delta >= 1, 1 <= K <= 256 (the paper's best K is 10).
+ *   dist (V words, device)          shortest distances; 0xFFFFFFFF =
+ *                                   unreachable.  Every shortest distance must
+ *                                   be < 2^32 - 1 (sums are saturated).
+ *   ws                              ms_sssp_workspace_size(V, E, K) bytes,
+ *                                   256-byte aligned (the work lists hold
+ *                                   2E + V + 1024 items; MS_ERR_WORKSPACE if a
+ *                                   graph ever needs more).
+ *   stats                           NULL or host struct: iterations, work-list
+ *                                   items multisplit, frontier items, pushes.
+ * SYNCHRONIZES `stream` once per iteration (the work-list length is read back),
+ * so it cannot be captured in a CUDA graph.
+ * --------------------------------------------------------------------- */
+typedef struct {
+  uint64_t iterations, items, frontier, pushes;
+} ms_sssp_stats;
+size_t ms_sssp_workspace_size(uint32_t V, uint64_t E, uint32_t K);
+ms_status ms_sssp(const uint32_t *row_ptr, const uint32_t *col, const uint32_t *w, uint32_t V,
+                  uint64_t E, uint32_t source, uint32_t delta, uint32_t K, uint32_t *dist, void *ws,
+                  size_t ws_bytes, void *stream, ms_sssp_stats *stats);
+
+/* ------------------------------------------------------------------------
  * Instrumentation (host only, thread-local, zero cost when unset).
  * --------------------------------------------------------------------- */
 

@@ -21,7 +21,7 @@ from ._lib import MultisplitError, check, ms_bucket_fn
 
 __all__ = ["Bucket", "Delta", "Identity", "Radix", "Splitters", "multisplit", "radix_sort", "device_status",
            "prescan", "scan", "tile_size", "radix_pass_schedule", "workspace_size",
-           "set_option", "get_option", "device_init", "MultisplitError"]
+           "set_option", "get_option", "device_init", "sssp", "MultisplitError"]
 
 
 @dataclass(frozen=True)
@@ -299,3 +299,32 @@ def histogram_range(samples: torch.Tensor, splitters: torch.Tensor, *, out: torc
                                         c.data_ptr(), _stream_ptr(stream))
     check(st, "ms_histogram_range")
     return c
+
+
+def sssp(row_ptr: torch.Tensor, col: torch.Tensor, weights: torch.Tensor, source: int, *,
+         delta: int = 100, buckets: int = 10, out: torch.Tensor | None = None,
+         workspace: torch.Tensor | None = None, stream=None, stats: bool = False):
+    """ms_sssp: Multisplit-SSSP (Sec.7.2): shortest distances from `source` on a CSR graph
+    (int32/uint32 CUDA tensors; weights >= 0) by delta-stepping whose bucketing is the
+    stable multisplit with `buckets` splitter buckets of width `delta`.  Returns dist
+    (uint32 bit patterns in an int32 tensor; 0xFFFFFFFF = unreachable), and the iteration
+    statistics if stats=True.  Synchronizes once per iteration."""
+    lib = _lib.load()
+    rp = _u32view(row_ptr, "row_ptr")
+    dv = rp.device
+    V = rp.numel() - 1
+    c = _u32view(col, "col", dv)
+    w = _u32view(weights, "weights", dv, c.numel())
+    E = c.numel()
+    d = _u32view(out, "out", dv, V) if out is not None else torch.empty(max(V, 0), dtype=torch.int32, device=dv)
+    ws = _workspace(workspace, lib.ms_sssp_workspace_size(V, E, buckets), dv)
+    st = _lib.ms_sssp_stats()
+    _prepare(rp)
+    with torch.cuda.device(dv):
+        check(lib.ms_sssp(rp.data_ptr(), c.data_ptr() if E else None, w.data_ptr() if E else None, V, E,
+                          source, delta, buckets, d.data_ptr(), ws.data_ptr(), ws.numel(),
+                          _stream_ptr(stream, dv), ctypes.byref(st)), "ms_sssp")
+    if stats:
+        return d, {"iterations": st.iterations, "items": st.items, "frontier": st.frontier,
+                   "pushes": st.pushes}
+    return d

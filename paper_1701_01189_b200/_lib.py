@@ -33,6 +33,11 @@ MS_BUCKET_RADIX = 2
 MS_BUCKET_SPLITTERS = 3
 
 
+class ms_sssp_stats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_uint64), ("items", ctypes.c_uint64),
+                ("frontier", ctypes.c_uint64), ("pushes", ctypes.c_uint64)]
+
+
 class ms_bucket_fn(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_uint32), ("num_buckets", ctypes.c_uint32),
                 ("delta", ctypes.c_uint32), ("shift", ctypes.c_uint32), ("bits", ctypes.c_uint32),
@@ -81,6 +86,8 @@ SIGNATURES = [
     ("ms_shard_workspace_size", _SZ, [_U64, _U32, _U32, _I]),
     ("ms_shard_prescan", _I, [_P, _U64, _FN, _I, _U32, _P, _P, _SZ, _P]),
     ("ms_shard_scatter", _I, [_P, _P, _U64, _FN, _P, _U32, _U32, _P, _P, _P, _P, _SZ, _P]),
+    ("ms_sssp_workspace_size", _SZ, [_U32, _U64, _U32]),
+    ("ms_sssp", _I, [_P, _P, _P, _U32, _U64, _U32, _U32, _U32, _P, _P, _SZ, _P, _P]),
     ("ms_set_stage_events", None, [_P]),
     ("ms_launch_count", _U64, []),
 ]
