@@ -55,7 +55,8 @@ __host__ __device__ inline size_t kmw_smem_bytes(uint32_t nb) {
 }
 __host__ __device__ inline size_t kfw_smem_bytes(bool pairs, uint32_t nb) {
   const uint32_t T = wide_tile(pairs);
-  return (3u * T * (pairs ? 2u : 1u) + wide_kw(pairs) * 16u * nb + 2u * 32u * nb) * 4u;
+  // 3 stages of [keys | values | record row 0], rank rows, 2 run tables, running offsets
+  return (3u * (T * (pairs ? 2u : 1u) + 16u * nb) + wide_kw(pairs) * 16u * nb + 2u * 32u * nb + 32u * nb) * 4u;
 }
 
 template <int NB>
@@ -279,7 +280,8 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   constexpr uint32_t kStages = 3, kPrefetch = 2;
   constexpr uint32_t HW = NB / 2, RW = 16u * NB, MP = 32u * NB;
   constexpr uint32_t REC = wide_rec_words(PAIRS, NB);
-  constexpr uint32_t SWD = T * (PAIRS ? 2u : 1u);  // words per stage
+  constexpr uint32_t SWD = T * (PAIRS ? 2u : 1u) + RW;  // words per stage: keys | values | record row 0
+  constexpr uint32_t R0 = T * (PAIRS ? 2u : 1u);        // offset of record row 0 in a stage
   using V = typename WideVec<NB>::T;
   extern __shared__ __align__(128) uint8_t kfw_raw[];
   __shared__ __align__(8) uint64_t bar[kStages];
@@ -287,6 +289,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kfw_raw);
   uint32_t *s_row = stage0 + kStages * SWD;  // [W][RW] packed running slots
   uint32_t *s_tab = s_row + W * RW;          // [2][MP] global minus tile offsets
+  uint32_t *s_grun = s_tab + 2u * MP;        // [MP] next global position of each bucket in this range
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr uint32_t kProducer = NT - 32;
 
@@ -296,14 +299,25 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   const uint32_t nt = t1 - t0;
   auto tile_n = [&](uint32_t t) { return min(T, a.n - t * T); };
   auto via_tma = [&](uint32_t t) { return a.use_tma && tile_n(t) == T; };
-  auto issue = [&](uint32_t t, uint32_t st) {
+  // one elected thread starts the TMA copies of a tile: the input (may run
+  // before griddep_wait: it predates KMW) and record row 0 (written by KMW:
+  // only after griddep_wait); one mbarrier transaction count for both
+  auto issue_data = [&](uint32_t t, uint32_t st) {
     if (tid == kProducer && t < t1 && via_tma(t)) {
       uint32_t *dst = stage0 + st * SWD;
       const uint64_t pol = policy_evict_first();
-      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u));
+      mbar_arrive_expect_tx(&bar[st], T * 4u * (PAIRS ? 2u : 1u) + RW * 4u);
       tma_load_1d(dst, a.keys_in + (size_t)t * T, T * 4u, &bar[st], pol);
       if constexpr (PAIRS) tma_load_1d(dst + T, a.vals_in + (size_t)t * T, T * 4u, &bar[st], pol);
     }
+  };
+  auto issue_rec = [&](uint32_t t, uint32_t st) {
+    if (tid == kProducer && t < t1 && via_tma(t))
+      tma_load_1d(stage0 + st * SWD + R0, a.meta + (size_t)t * REC, RW * 4u, &bar[st], policy_evict_first());
+  };
+  auto issue = [&](uint32_t t, uint32_t st) {
+    issue_data(t, st);
+    issue_rec(t, st);
   };
   auto prefetch = [&](uint32_t t, bool meta) {
     if (tid == kProducer && t < t1) {
@@ -318,13 +332,13 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   if (tid == 0)
     for (uint32_t i = 0; i < kStages; ++i) mbar_init(&bar[i], 1);
   __syncthreads();
-  issue(t0, 0);
-  issue(t0 + 1, 1);
+  issue_data(t0, 0);
+  issue_data(t0 + 1, 1);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, false);
 
   uint32_t key[ITEMS];
   uint32_t val[PAIRS ? ITEMS : 1];
-  uint32_t mrow[HW], mrow0[HW];  // this warp's record row and row 0 (packed 16-bit)
+  uint32_t mrow[HW];  // this warp's record row (packed 16-bit)
   const uint32_t wbase = warp * (ITEMS * 32);
   auto load_tile = [&](uint32_t t, uint32_t k) {
     const uint32_t st = k % kStages;
@@ -332,7 +346,6 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
     const uint32_t tn = tile_n(t);
     const uint32_t *rec = a.meta + (size_t)t * REC;
     wide_unpack<NB>(__ldcg(reinterpret_cast<const V *>(rec + warp * RW) + lane), mrow);
-    wide_unpack<NB>(__ldcg(reinterpret_cast<const V *>(rec) + lane), mrow0);
     if (via_tma(t)) {
       mbar_wait(&bar[st], (k / kStages) & 1u);
 #pragma unroll
@@ -356,9 +369,11 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
   // bucket totals; base[b] = exclusive scan of the totals
   griddep_wait();  // KM and KR complete
   if (a.npeers && tid <= a.npeers) s_ps[tid] = __ldcg(a.peer_start + tid);
+  issue_rec(t0, 0);
+  issue_rec(t0 + 1, 1);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, true);
-  uint32_t grun[NB];  // next global position of each bucket of this lane in this range
-  {
+  if (warp == W - 1) {  // the running offsets live in shared memory, kept by the last warp
+    uint32_t grun[NB];
     const uint32_t c = blockIdx.x;
     uint32_t tot[NB], s = 0;
 #pragma unroll
@@ -378,11 +393,12 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
       grun[j] += incl - s;
       const uint32_t b = lane * NB + j;
       if (a.gbase_ovr) grun[j] = b < bp.m ? __ldcg(a.gbase_ovr + b) : 0u;
-      if (c == 0 && warp == 0 && a.bucket_offsets) {
+      if (c == 0 && a.bucket_offsets) {
         if (b < bp.m) a.bucket_offsets[b] = grun[j];
         if (b + 1 == bp.m) a.bucket_offsets[bp.m] = grun[j] + tot[j];
       }
       grun[j] += __ldcg(a.R + (size_t)c * MP + b);
+      s_grun[b] = grun[j];
     }
   }
   load_tile(t0, 0);
@@ -398,19 +414,26 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
 
     // ---- per-warp setup: running slots of this warp's buckets; the tile's
     // global offsets (Eq.3 term 3: grun accumulates the range's earlier tiles)
-    {
-      uint32_t tb[NB];
+    if (warp == W - 1) {
+      // record row 0 = the tile's bucket bases: from the stage (TMA) or global
+      const uint32_t *r0 = via_tma(t) ? s_stage + R0 : a.meta + (size_t)t * REC;
+      uint32_t mrow0[HW], tb[NB], g[NB];
+      wide_unpack<NB>(via_tma(t) ? reinterpret_cast<const V *>(r0)[lane]
+                                 : __ldcg(reinterpret_cast<const V *>(r0) + lane), mrow0);
 #pragma unroll
       for (int j = 0; j < NB; ++j) tb[j] = (mrow0[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+      ld_words<NB>(s_grun + lane * NB, g);
       const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, tb[0], 1);
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const uint32_t te = j + 1 < NB ? tb[j + 1] : (lane < 31 ? nxt : tn);
-        if (warp == W - 1) tab[lane * NB + j] = grun[j] - tb[j];
-        grun[j] += te - tb[j];
+        tab[lane * NB + j] = g[j] - tb[j];
+        g[j] += te - tb[j];
       }
-      reinterpret_cast<V *>(brow)[lane] = wide_pack<NB>(mrow);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) s_grun[lane * NB + j] = g[j];
     }
+    reinterpret_cast<V *>(brow)[lane] = wide_pack<NB>(mrow);
     __syncwarp();
 
     // ---- rank and place: slot = lane-ordered increment of the packed 16-bit
@@ -462,40 +485,45 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
       prefetch(t + 2 + kPrefetch, true);
     }
 
-    // ---- coalesced scatter of tile t: slot s of bucket b -> tab[b] + s --------
+    // ---- coalesced scatter of tile t: slot s of bucket b -> tab[b] + s, in
+    // chunks of 8 slots per thread (fewer live registers than all 16 at once)
     {
       const uint32_t s0 = wbase + lane;
-      uint32_t kk[ITEMS], pos[ITEMS];
+      constexpr uint32_t CH = 8;
 #pragma unroll
-      for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[s0 + 32 * i];
+      for (uint32_t c = 0; c < ITEMS; c += CH) {
+        uint32_t kk[CH], pos[CH];
 #pragma unroll
-      for (int i = 0; i < (int)ITEMS; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * i;
-      if (a.npeers) {  // sharded: into the owning rank's window (KP)
+        for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[s0 + 32 * (c + i)];
 #pragma unroll
-        for (int i = 0; i < (int)ITEMS; ++i)
-          if (s0 + 32 * i < tn)
-            kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[T + s0 + 32 * i] : 0u);
-      } else if (tn == T) {  // full tile: no per-element predicates
-        uint32_t *__restrict__ ko = a.keys_out;
+        for (uint32_t i = 0; i < CH; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * (c + i);
+        if (a.npeers) {  // sharded: into the owning rank's window (KP)
 #pragma unroll
-        for (int i = 0; i < (int)ITEMS; ++i) ko[pos[i]] = kk[i];
-        if constexpr (PAIRS) {
-          uint32_t *__restrict__ vo = a.vals_out;
+          for (uint32_t i = 0; i < CH; ++i)
+            if (s0 + 32 * (c + i) < tn)
+              kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[T + s0 + 32 * (c + i)] : 0u);
+        } else if (tn == T) {  // full tile: no per-element predicates
+          uint32_t *__restrict__ ko = a.keys_out;
 #pragma unroll
-          for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[T + s0 + 32 * i];
+          for (uint32_t i = 0; i < CH; ++i) ko[pos[i]] = kk[i];
+          if constexpr (PAIRS) {
+            uint32_t *__restrict__ vo = a.vals_out;
 #pragma unroll
-          for (int i = 0; i < (int)ITEMS; ++i) vo[pos[i]] = kk[i];
-        }
-      } else {
+            for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[T + s0 + 32 * (c + i)];
 #pragma unroll
-        for (int i = 0; i < (int)ITEMS; ++i)
-          if (s0 + 32 * i < tn) a.keys_out[pos[i]] = kk[i];
-        if constexpr (PAIRS) {
+            for (uint32_t i = 0; i < CH; ++i) vo[pos[i]] = kk[i];
+          }
+        } else {
 #pragma unroll
-          for (int i = 0; i < (int)ITEMS; ++i) kk[i] = s_stage[T + s0 + 32 * i];
+          for (uint32_t i = 0; i < CH; ++i)
+            if (s0 + 32 * (c + i) < tn) a.keys_out[pos[i]] = kk[i];
+          if constexpr (PAIRS) {
 #pragma unroll
-          for (int i = 0; i < (int)ITEMS; ++i)
-            if (s0 + 32 * i < tn) a.vals_out[pos[i]] = kk[i];
+            for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[T + s0 + 32 * (c + i)];
+#pragma unroll
+            for (uint32_t i = 0; i < CH; ++i)
+              if (s0 + 32 * (c + i) < tn) a.vals_out[pos[i]] = kk[i];
+          }
         }
       }
     }
