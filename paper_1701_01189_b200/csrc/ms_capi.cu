@@ -310,6 +310,7 @@ cudaError_t fused(const Plan &pl, bool pairs, const KfArgs &a, uint32_t grid, cu
 struct L0 {
   bool wide;
   uint32_t G, K, mP, num_tiles;
+  uint32_t GM, KM;  // prescan CTAs and their tiles: KM = K, or K / 2 (two per range)
   uint32_t *R, *P, *Tot, *meta;
 };
 
@@ -331,16 +332,20 @@ L0 l0_setup(uint32_t m, bool pairs, const Layout &lo, char *w) {
     st.meta = (uint32_t *)(w + lo.meta);
     return st;
   }
-  // K even for pairs so that a KM tile (8192 keys = two pair tiles) never
-  // straddles two ranges
+  // the KM tile is the KF tile (ms_wide.cuh); one range per postscan CTA.
+  // Pairs run one postscan CTA per SM but two prescan CTAs (each half a
+  // range, K even): R and its column prefix P have a row per prescan CTA and
+  // range c starts at row 2c
   st.mP = 32u * lo.NB;
-  const uint32_t target = std::min((uint32_t)sm_count() * 2u, kMaxRanges);
+  const uint32_t target = std::min((uint32_t)sm_count() * wide_ctas_per_sm(pairs), kMaxRanges);
   st.K = (lo.LW + target - 1) / target;
   if (pairs && (st.K & 1u)) ++st.K;
   st.G = (lo.LW + st.K - 1) / st.K;
+  st.KM = pairs ? st.K / 2u : st.K;
+  st.GM = (lo.LW + st.KM - 1) / st.KM;
   st.num_tiles = lo.LW;
   st.R = H;
-  st.P = H + (size_t)st.G * st.mP;
+  st.P = H + (size_t)st.GM * st.mP;
   st.meta = (uint32_t *)(w + lo.wmeta);
   return st;
 }
@@ -358,10 +363,8 @@ cudaError_t l0_prescan(const Plan &pl, bool pairs, const uint32_t *keys, uint32_
       e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.G, m, s));
     return e;
   }
-  const uint32_t per_km = pairs ? st.K / 2u : st.K;
-  const uint32_t LM = (uint32_t)((n + kWideKmTile - 1) / kWideKmTile);
-  cudaError_t e = counted(tile_meta_wide(pl, pairs, keys, n, LM, per_km, st.G, st.meta, lo.LW, st.R, hdr, s));
-  if (e == cudaSuccess) e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.G, st.mP, s));
+  cudaError_t e = counted(tile_meta_wide(pl, pairs, keys, n, lo.LW, st.KM, st.GM, st.meta, lo.LW, st.R, hdr, s));
+  if (e == cudaSuccess) e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.GM, st.mP, s));
   return e;
 }
 
@@ -377,6 +380,7 @@ cudaError_t l0_postscan(const Plan &pl, bool pairs, KfArgs &a, const L0 &st, cud
   }
   a.R = st.P;
   a.Tot = st.Tot;
+  a.prefix_step = st.KM == st.K ? 1u : 2u;
   return counted(fused_meta_wide(pl, pairs, a, st.G, s));
 }
 

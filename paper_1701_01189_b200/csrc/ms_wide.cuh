@@ -8,8 +8,8 @@
 //       memory atomic unit, so a 90 % hot bucket costs nothing); one scan warp turns them into tile meta records
 //       S[w][b] = sum_{b'<b} h_b' + sum_{w'<w} c_{w',b}  (Eq.4 terms 2-3,
 //       P:952-955), stored as 16-bit slot bases, and accumulates the range
-//       histograms R[c][b] (the level-0 column of Eq.3).  For pairs the KF tile
-//       is 4096 elements (8 warp slices), so a KM tile yields two records.
+//       histograms R[c][b] (the level-0 column of Eq.3).  The KM tile is the
+//       KF tile (8192 keys or pairs, 16 warp slices of 512).
 //   KR  kr_level0_scan (ms_kernels.cuh): P[c][b] = sum_{c'<c} R[c'][b], totals.
 //   KFW kf_meta_wide (postscan): persistent CTA per level-0 range,
 //       tiles in order; each warp takes its slot bases from its record row,
@@ -38,8 +38,13 @@ namespace ms {
 __host__ __device__ constexpr uint32_t wide_nb(uint32_t m) {
   return m <= 64 ? 2u : (m <= 128 ? 4u : 8u);
 }
-// KF tile and its warp count: keys 16 warps x 16 windows, pairs 8 x 16
-__host__ __device__ constexpr uint32_t wide_kw(bool pairs) { return pairs ? 8u : 16u; }
+// KF tile and its warp count: 16 warps x 16 windows (8192 keys or pairs).
+// Pairs run one CTA per SM (128 registers, 3 stages of 64 KB): measured, the
+// postscan's DRAM efficiency follows the length of the bucket runs a tile
+// writes (T/m elements): 4096-pair tiles (two CTAs per SM) wrote runs of 16
+// and reached 2.3 TB/s at m = 256, against 3.1 TB/s at runs of 32 (m = 128)
+__host__ __device__ constexpr uint32_t wide_kw(bool) { return 16u; }
+__host__ __device__ constexpr uint32_t wide_ctas_per_sm(bool pairs) { return pairs ? 1u : 2u; }
 __host__ __device__ constexpr uint32_t wide_tile(bool pairs) { return 32u * 16u * wide_kw(pairs); }
 // record: KW rows of mP 16-bit slot bases
 __host__ __device__ constexpr uint32_t wide_rec_words(bool pairs, uint32_t nb) {
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
 //   the last warp refills the stage of tile t-1 with tile t+2.
 // ============================================================================
 template <int KIND, bool PAIRS, int NB>
-__global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a, BucketParams bp) {
+__global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) kf_meta_wide(KfArgs a, BucketParams bp) {
   MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   constexpr uint32_t W = wide_kw(PAIRS), NT = W * 32, ITEMS = 16;
   constexpr uint32_t T = NT * ITEMS;
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, 2) kf_meta_wide(KfArgs a,
         if (b < bp.m) a.bucket_offsets[b] = grun[j];
         if (b + 1 == bp.m) a.bucket_offsets[bp.m] = grun[j] + tot[j];
       }
-      grun[j] += __ldcg(a.R + (size_t)c * MP + b);
+      grun[j] += __ldcg(a.R + (size_t)c * a.prefix_step * MP + b);
       s_grun[b] = grun[j];
     }
   }
