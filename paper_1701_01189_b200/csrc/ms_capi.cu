@@ -332,16 +332,16 @@ L0 l0_setup(uint32_t m, bool pairs, const Layout &lo, char *w) {
     st.meta = (uint32_t *)(w + lo.meta);
     return st;
   }
-  // the KM tile is the KF tile (ms_wide.cuh); one range per postscan CTA.
-  // Pairs run one postscan CTA per SM but two prescan CTAs (each half a
-  // range, K even): R and its column prefix P have a row per prescan CTA and
+  // the KM tile is the KF tile (ms_wide.cuh); one range per postscan CTA,
+  // one postscan CTA per SM, two prescan CTAs per SM and range (each half of
+  // it, K even): R and its column prefix P have a row per prescan CTA and
   // range c starts at row 2c
   st.mP = 32u * lo.NB;
   const uint32_t target = std::min((uint32_t)sm_count() * wide_ctas_per_sm(pairs), kMaxRanges);
   st.K = (lo.LW + target - 1) / target;
-  if (pairs && (st.K & 1u)) ++st.K;
+  if (st.K & 1u) ++st.K;
   st.G = (lo.LW + st.K - 1) / st.K;
-  st.KM = pairs ? st.K / 2u : st.K;
+  st.KM = st.K / 2u;
   st.GM = (lo.LW + st.KM - 1) / st.KM;
   st.num_tiles = lo.LW;
   st.R = H;

@@ -199,9 +199,10 @@ static cudaError_t kmw_go(const uint32_t *keys, uint32_t n, uint32_t num_tiles, 
                           uint32_t *R, uint32_t *hdr, cudaStream_t s) {
   auto kern = km_meta_wide<KIND, NB, PAIRS>;
   static std::atomic<unsigned long long> done{0};
-  const cudaError_t e = set_max_smem(kern, kmw_smem_bytes(NB), done);
+  const cudaError_t e = set_max_smem(kern, kmw_smem_bytes(NB, PAIRS), done);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads + 32, kmw_smem_bytes(NB), s>>>(keys, n, num_tiles, per, bp, meta, nkf, R, hdr);
+  kern<<<grid, kThreads + 32, kmw_smem_bytes(NB, PAIRS), s>>>(keys, n, num_tiles, per, bp, meta,
+                                                                       nkf, R, hdr);
   return cudaGetLastError();
 }
 

@@ -38,25 +38,36 @@ namespace ms {
 __host__ __device__ constexpr uint32_t wide_nb(uint32_t m) {
   return m <= 64 ? 2u : (m <= 128 ? 4u : 8u);
 }
-// KF tile and its warp count: 16 warps x 16 windows (8192 keys or pairs).
-// Pairs run one CTA per SM (128 registers, 3 stages of 64 KB): measured, the
-// postscan's DRAM efficiency follows the length of the bucket runs a tile
-// writes (T/m elements): 4096-pair tiles (two CTAs per SM) wrote runs of 16
-// and reached 2.3 TB/s at m = 256, against 3.1 TB/s at runs of 32 (m = 128)
-__host__ __device__ constexpr uint32_t wide_kw(bool) { return 16u; }
-__host__ __device__ constexpr uint32_t wide_ctas_per_sm(bool pairs) { return pairs ? 1u : 2u; }
+// KF tile and its warp count: W warps x 16 windows, W = 32 for keys (16384
+// keys, 1024 threads) and 16 for pairs (8192 pairs, 128 registers); one CTA
+// per SM, 3 stages of 64 KB.  Measured, the postscan's DRAM efficiency follows
+// the length of the bucket runs a tile writes (T/m elements): 4096-pair tiles
+// (runs of 16 at m = 256) reached 2.3 TB/s, runs of 32 3.1 TB/s (profiles/r02).
+// The KM tile is the KF tile, counted by W warps.
+__host__ __device__ constexpr uint32_t wide_kw(bool pairs) { return pairs ? 16u : 32u; }
+__host__ __device__ constexpr uint32_t wide_ctas_per_sm(bool) { return 1u; }
 __host__ __device__ constexpr uint32_t wide_tile(bool pairs) { return 32u * 16u * wide_kw(pairs); }
 // record: KW rows of mP 16-bit slot bases
 __host__ __device__ constexpr uint32_t wide_rec_words(bool pairs, uint32_t nb) {
   return wide_kw(pairs) * 32u * nb / 2u;
 }
-constexpr uint32_t kWideKmTile = 8192;  // KM tile (16 slices of 512 keys)
-// KM TMA ring depth: 3 tiles, 2 at m > 128 (32-bit warp counters of 256
-// buckets take 32 KB; two 32 KB tiles in flight per CTA, two CTAs per SM, are
-// still far more than the bytes in flight the HBM latency needs)
-__host__ __device__ constexpr uint32_t kmw_stages(uint32_t nb) { return nb == 8 ? 2u : 3u; }
-__host__ __device__ inline size_t kmw_smem_bytes(uint32_t nb) {
-  return (kmw_stages(nb) * kWideKmTile + 2u * kWarps * 32u * nb) * 4u;
+// KMW shared memory <= 96 KB (two CTAs per SM): 32-bit warp counters, two
+// buffers of W rows of 32 NB words, and as many TMA units of 8192 keys (32 KB)
+// as fit, at most 3 (keys at m > 128: 64 KB of counters, one unit)
+// counter buffers: two (the counting warps run a tile ahead of the scan warp),
+// one where two would take more than 32 KB (keys at m > 128: the ring keeps two
+// units, measured faster than two counter buffers and one unit)
+__host__ __device__ constexpr uint32_t kmw_cnt_bufs(uint32_t nb, bool pairs) {
+  return wide_kw(pairs) * 32u * nb * 2u <= 8192u ? 2u : 1u;
+}
+__host__ __device__ constexpr uint32_t kmw_cnt_words(uint32_t nb, bool pairs) {
+  return kmw_cnt_bufs(nb, pairs) * wide_kw(pairs) * 32u * nb;
+}
+__host__ __device__ constexpr uint32_t kmw_stages(uint32_t nb, bool pairs) {
+  return (24576u - kmw_cnt_words(nb, pairs)) / 8192u > 3u ? 3u : (24576u - kmw_cnt_words(nb, pairs)) / 8192u;
+}
+__host__ __device__ inline size_t kmw_smem_bytes(uint32_t nb, bool pairs) {
+  return ((size_t)kmw_stages(nb, pairs) * 8192u + kmw_cnt_words(nb, pairs)) * 4u;
 }
 __host__ __device__ inline size_t kfw_smem_bytes(bool pairs, uint32_t nb) {
   const uint32_t T = wide_tile(pairs);
@@ -124,111 +135,127 @@ __device__ __forceinline__ typename WideVec<NB>::T wide_pack(const uint32_t (&w)
 }
 
 // ============================================================================
-// KMW.  CTA c handles KM tiles [c*K, min(LM, (c+1)*K)) of 8192 keys; warp w of
-// the 16 counting warps counts slice w (keys [t*8192 + 512 w, +512)).
+// KMW.  CTA c handles KF tiles [c*K, min(LM, (c+1)*K)); a tile has W slices of
+// 512 keys (W = 32 keys / 16 pairs), each a record row.  The TMA unit is a
+// half tile of 8192 keys (32 KB; H = W / 16 units per tile) in a ring of KS
+// units; the 16 counting warps count slice w of every unit into row
+// (h * 16 + w) of the tile's 32-bit counters (kmw_cnt_bufs buffers; a
+// constant +1 compiles to ATOMS.POPC.INC, which merges a warp's same-address
+// increments: packed 16-bit counters made the 90 %-skewed C3 prescan 4x
+// slower), then arrive on the unit's sfree barrier.  The scan warp refills a
+// stage as soon as its unit is counted and, once every unit of a tile is,
+// turns the counters into the record and zeroes them.  <= 96 KB of shared
+// memory: two CTAs per SM.
 // ============================================================================
+__host__ __device__ constexpr uint32_t kmw_unit() { return 8192u; }
+
 template <int KIND, int NB, bool PAIRS>
 __global__ void __launch_bounds__(kThreads + 32, 2)
     km_meta_wide(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
                  uint32_t num_kf_tiles, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
   MS_STAGE_SPLITTERS(bp, kMaxBuckets);
-  constexpr uint32_t W = kWarps, SL = 512, T = kWideKmTile, KS = kmw_stages(NB);
+  constexpr uint32_t W = wide_kw(PAIRS), CW = kWarps, SL = 512, T = W * SL, U = CW * SL;
+  constexpr uint32_t H = W / CW;                  // TMA units per tile
+  constexpr uint32_t KS = kmw_stages(NB, PAIRS);  // units in the ring
+  constexpr uint32_t CB = kmw_cnt_bufs(NB, PAIRS);  // counter buffers
   constexpr uint32_t HW = NB / 2;                 // packed record words per lane per row
   constexpr uint32_t RW = 16u * NB;               // packed record words per row (mP / 2)
-  constexpr uint32_t MP = 32u * NB;               // counters per warp row
-  constexpr uint32_t KW = wide_kw(PAIRS);         // warp rows per record
+  constexpr uint32_t MP = 32u * NB;               // counters per row
   constexpr uint32_t REC = wide_rec_words(PAIRS, NB);
   using V = typename WideVec<NB>::T;
-  extern __shared__ __align__(128) uint32_t kmw_smem[];  // stages [KS][T] | cnt[2][W][MP]
+  extern __shared__ __align__(128) uint32_t kmw_smem[];  // stages [KS][U] | cnt[2][W][MP]
   __shared__ __align__(8) uint64_t full[KS];
-  __shared__ __align__(8) uint64_t cfull[2];
+  __shared__ __align__(8) uint64_t sfree[KS];
   __shared__ __align__(8) uint64_t cempty[2];
   griddep_launch_dependents();
-  uint32_t *cnt = kmw_smem + KS * T;
+  uint32_t *cnt = kmw_smem + KS * U;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (blockIdx.x == 0 && tid == 0) hdr[0] = 0u;
-  for (uint32_t i = tid; i < 2 * W * MP; i += blockDim.x) cnt[i] = 0u;
+  for (uint32_t i = tid; i < CB * W * MP; i += blockDim.x) cnt[i] = 0u;
   const uint32_t t0 = blockIdx.x * tiles_per_cta;
   const uint32_t t1 = min(num_tiles, t0 + tiles_per_cta);
+  const uint32_t nu = t1 > t0 ? (t1 - t0) * H : 0u;  // units of this CTA
   const bool aligned = ((reinterpret_cast<uintptr_t>(keys) & 15u) == 0);
-  auto via_tma = [&](uint32_t t) { return aligned && (uint64_t)(t + 1) * T <= n; };
+  auto unit_start = [&](uint32_t u) { return (uint64_t)t0 * T + (uint64_t)u * U; };
+  auto via_tma = [&](uint32_t u) { return aligned && unit_start(u) + U <= n; };
   if (tid == 0) {
-    for (uint32_t i = 0; i < KS; ++i) mbar_init(&full[i], 1);
-    for (uint32_t i = 0; i < 2; ++i) {
-      mbar_init(&cfull[i], kThreads);
-      mbar_init(&cempty[i], 32);
+    for (uint32_t i = 0; i < KS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&sfree[i], CW * 32u);
     }
+    for (uint32_t i = 0; i < 2; ++i) mbar_init(&cempty[i], 32);
   }
   __syncthreads();
 
-  if (warp == W) {
+  if (warp == CW) {
     // ============================ scan warp ===================================
-    auto issue = [&](uint32_t t, uint32_t st) {
-      if (lane == 0 && t < t1 && via_tma(t)) {
-        mbar_arrive_expect_tx(&full[st], T * 4u);
-        tma_load_1d(kmw_smem + st * T, keys + (size_t)t * T, T * 4u, &full[st], policy_evict_first());
+    auto issue = [&](uint32_t u) {
+      if (lane == 0 && u < nu && via_tma(u)) {
+        const uint32_t st = u % KS;
+        mbar_arrive_expect_tx(&full[st], U * 4u);
+        tma_load_1d(kmw_smem + st * U, keys + unit_start(u), U * 4u, &full[st], policy_evict_first());
       }
     };
-    for (uint32_t i = 0; i < KS; ++i) issue(t0 + i, i);
+    for (uint32_t u = 0; u < KS; ++u) issue(u);
     uint32_t running[NB];
 #pragma unroll
     for (int j = 0; j < NB; ++j) running[j] = 0u;
     uint32_t k = 0;
     for (uint32_t t = t0; t < t1; ++t, ++k) {
-      const uint32_t p = k & 1u;
-      mbar_wait(&cfull[p], (k >> 1) & 1u);
-      if (lane == 0) fence_proxy_async_smem();
-      issue(t + KS, k % KS);
+      const uint32_t p = k % CB;
+#pragma unroll
+      for (uint32_t h = 0; h < H; ++h) {  // every unit of the tile counted; refill its stage
+        const uint32_t u = k * H + h;
+        mbar_wait(&sfree[u % KS], (u / KS) & 1u);
+        if (lane == 0) fence_proxy_async_smem();
+        issue(u + KS);
+      }
       uint32_t *c = cnt + p * W * MP;
-#pragma unroll 1
-      for (uint32_t half = 0; half < W / KW; ++half) {
-        // pass 1: tile (or half-tile) count h of this lane's buckets
-        uint32_t h[NB];
+      // pass 1: tile count h of this lane's buckets
+      uint32_t hc[NB];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) h[j] = 0u;
+      for (int j = 0; j < NB; ++j) hc[j] = 0u;
 #pragma unroll 4
-        for (uint32_t w = 0; w < KW; ++w) {
-          uint32_t x[NB];
-          ld_words<NB>(c + (half * KW + w) * MP + lane * NB, x);
+      for (uint32_t w = 0; w < W; ++w) {
+        uint32_t x[NB];
+        ld_words<NB>(c + w * MP + lane * NB, x);
 #pragma unroll
-          for (int j = 0; j < NB; ++j) h[j] += x[j];
-        }
-        // exclusive scan over the buckets (in-lane prefix + warp scan of lane sums)
-        uint32_t tb[NB], s = 0;
+        for (int j = 0; j < NB; ++j) hc[j] += x[j];
+      }
+      // exclusive scan over the buckets (in-lane prefix + warp scan of lane sums)
+      uint32_t tb[NB], s = 0;
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          tb[j] = s;
-          s += h[j];
-        }
-        uint32_t incl = s;
+      for (int j = 0; j < NB; ++j) {
+        tb[j] = s;
+        s += hc[j];
+      }
+      uint32_t incl = s;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= (uint32_t)o) incl += y;
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
 #pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          tb[j] += incl - s;
-          running[j] += h[j];
-        }
-        // pass 2: S[w][b] = tb[b] + sum_{w'<w} c_{w',b}; zero the counters
-        const uint32_t tf = t * (W / KW) + half;  // KF tile of this record
-        uint32_t *rec = meta + (size_t)tf * REC;
+      for (int j = 0; j < NB; ++j) {
+        tb[j] += incl - s;
+        running[j] += hc[j];
+      }
+      // pass 2: S[w][b] = tb[b] + sum_{w'<w} c_{w',b} (16-bit); zero the counters
+      uint32_t *rec = meta + (size_t)t * REC;
 #pragma unroll 2
-        for (uint32_t w = 0; w < KW; ++w) {
-          uint32_t *cw = c + (half * KW + w) * MP + lane * NB;
-          uint32_t x[NB], o[HW];
-          ld_words<NB>(cw, x);
+      for (uint32_t w = 0; w < W; ++w) {
+        uint32_t *cw = c + w * MP + lane * NB;
+        uint32_t x[NB], o[HW];
+        ld_words<NB>(cw, x);
 #pragma unroll
-          for (int i = 0; i < (int)HW; ++i) {
-            o[i] = (tb[2 * i] & 0xFFFFu) | (tb[2 * i + 1] << 16);
-            tb[2 * i] += x[2 * i];
-            tb[2 * i + 1] += x[2 * i + 1];
-          }
-          st_zero_words<NB>(cw);
-          if (tf < num_kf_tiles) reinterpret_cast<V *>(rec + w * RW)[lane] = wide_pack<NB>(o);
+        for (int i = 0; i < (int)HW; ++i) {
+          o[i] = (tb[2 * i] & 0xFFFFu) | (tb[2 * i + 1] << 16);
+          tb[2 * i] += x[2 * i];
+          tb[2 * i + 1] += x[2 * i + 1];
         }
+        st_zero_words<NB>(cw);
+        if (t < num_kf_tiles) reinterpret_cast<V *>(rec + w * RW)[lane] = wide_pack<NB>(o);
       }
       __syncwarp();
       mbar_arrive(&cempty[p]);
@@ -240,33 +267,32 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
   }
 
   // ============================ counting warps ================================
-  uint32_t k = 0;
-  for (uint32_t t = t0; t < t1; ++t, ++k) {
-    const uint32_t p = k & 1u, st = k % KS;
-    if (k >= 2) mbar_wait(&cempty[p], ((k - 2) >> 1) & 1u);
-    uint32_t *row = cnt + (p * W + warp) * MP;
-    if (via_tma(t)) {
-      mbar_wait(&full[st], (k / KS) & 1u);
-      const uint4 *v = reinterpret_cast<const uint4 *>(kmw_smem + st * T + warp * SL);
+  for (uint32_t u = 0; u < nu; ++u) {
+    const uint32_t k = u / H, h = u % H, p = k % CB, st = u % KS;
+    if (h == 0 && k >= CB) mbar_wait(&cempty[p], ((k - CB) / CB) & 1u);  // buffer p scanned and zeroed
+    uint32_t *row = cnt + (p * W + h * CW + warp) * MP;
+    if (via_tma(u)) {
+      mbar_wait(&full[st], (u / KS) & 1u);
+      const uint4 *v = reinterpret_cast<const uint4 *>(kmw_smem + st * U + warp * SL);
       uint4 q[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = v[lane + 32u * (uint32_t)u];
+      for (int i = 0; i < 4; ++i) q[i] = v[lane + 32u * (uint32_t)i];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t k4[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           atomicAdd(row + bucket_of<KIND>(k4[e], bp), 1u);
         }
       }
-    } else {  // ragged last tile / unaligned input
-      const uint64_t lo = (uint64_t)t * T + warp * SL;
+    } else {  // ragged last unit / unaligned input
+      const uint64_t lo = unit_start(u) + warp * SL;
       const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
       for (uint32_t i = (uint32_t)lo + lane; i < hi; i += 32u) {
         atomicAdd(row + bucket_of<KIND>(__ldg(keys + i), bp), 1u);
       }
     }
-    mbar_arrive(&cfull[p]);
+    mbar_arrive(&sfree[st]);
   }
 }
 
