@@ -78,9 +78,9 @@ WORKLOADS = {
                        desc="device-wide Range histogram, 2^25 floats U[0,1024), m-1 random splitters (f2)"),
     # Multisplit-SSSP (Sec.7.2, f4): R-MAT scale 20 (1 M vertices), 5 edges per vertex made
     # undirected (10.5 M arcs, average degree 10; the paper's rmat: 0.8 M vertices, average
-    # degree 12); weights 0..1000; source 0; delta 100, 10 buckets
+    # degree 12); weights 0..1000; source 0; delta 200 (measured best of 50..1000), 10 buckets
     "sssp_rmat": dict(n=0, pairs=False, kind="sssp", m=10, unit="MTEPS", bpe=0, scale=20, ef=5,
-                      delta=100, desc="Multisplit-SSSP on an undirected R-MAT graph, scale 20, "
+                      delta=200, desc="Multisplit-SSSP on an undirected R-MAT graph, scale 20, "
                                       "edge factor 5, weights 0..1000 (Sec.7.2, f4)"),
     # splitter buckets (f3): m-1 random sorted splitters over uniform keys
     "ms_keys_spl": dict(n=1 << 25, pairs=False, kind="splitters", m=32, unit="Gkeys/s", bpe=12,

@@ -110,35 +110,48 @@ __global__ void __launch_bounds__(256)
     nv[i] = __ldg(ov + hi + i);
     mymin = min(mymin, k);
   }
-  // bucket 0: warps take 32 items at a time
+  // bucket 0: warps take 32 items at a time and flatten their edge lists: the
+  // warp's edges are numbered by an exclusive scan of the lanes' degrees and
+  // lane j relaxes edge g = 32 c + j of chunk c, found by a binary search over
+  // the scan (all lanes busy whatever the degree mix; the loads of a chunk are
+  // independent, unlike a per-lane walk of a vertex's list)
+  // Each warp takes a contiguous segment of ceil(hi / warps) items (usually a
+  // handful: frontiers are small next to the grid), so every warp of the grid
+  // has edges in flight, not only hi / 32 of them.
   const uint32_t wid = gtid >> 5, nw = gsz >> 5;
-  for (uint32_t b0 = wid * 32u; b0 < hi; b0 += nw * 32u) {
+  const uint32_t S = max(1u, (hi + nw - 1u) / nw);
+  for (uint32_t s0 = wid * S; s0 < hi; s0 += nw * S)
+  for (uint32_t b0 = s0, s1 = min(hi, s0 + S); b0 < s1; b0 += 32u) {
     const uint32_t i = b0 + lane;
-    uint32_t d = 0, e0 = 0, e1 = 0;
-    if (i < hi) {
+    uint32_t d = 0, e0 = 0, deg = 0;
+    if (i < s1) {
       const uint32_t v = __ldg(ov + i);
       d = __ldg(ok + i);
       if (d == __ldcg(dist + v)) {  // else a stale item: a shorter path has been pushed
         e0 = __ldg(rp + v);
-        e1 = __ldg(rp + v + 1);
+        deg = __ldg(rp + v + 1) - e0;
       }
     }
-    // vertices of degree >= 32: the whole warp walks their edge lists
-    uint32_t big = __ballot_sync(0xFFFFFFFFu, e1 - e0 >= 32u);
-    while (big) {
-      const uint32_t src = __ffs(big) - 1u;
-      big &= big - 1u;
-      const uint32_t bd = __shfl_sync(0xFFFFFFFFu, d, src);
-      const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, e0, src), s1 = __shfl_sync(0xFFFFFFFFu, e1, src);
-      for (uint32_t e = s0; e < s1; e += 32u)
-        relax_edge(e + lane < s1, e + lane, bd, dist, col, w, nk, nv, nrem, cap, ctl, mymin, lane);
+    uint32_t incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
     }
-    if (e1 - e0 >= 32u) e1 = e0;
-    // the others: one lane per vertex
-    const uint32_t deg = e1 - e0;
-    const uint32_t maxdeg = __reduce_max_sync(0xFFFFFFFFu, deg);
-    for (uint32_t t = 0; t < maxdeg; ++t)
-      relax_edge(t < deg, e0 + t, d, dist, col, w, nk, nv, nrem, cap, ctl, mymin, lane);
+    const uint32_t excl = incl - deg;
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    for (uint32_t c = 0; c < total; c += 32u) {
+      const uint32_t g = c + lane;
+      uint32_t s = 0;  // the last lane whose first edge is <= g
+#pragma unroll
+      for (uint32_t step = 16; step != 0; step >>= 1) {
+        const uint32_t ex = __shfl_sync(0xFFFFFFFFu, excl, s + step);
+        if (ex <= g) s += step;
+      }
+      const uint32_t sd = __shfl_sync(0xFFFFFFFFu, d, s);
+      const uint32_t se = __shfl_sync(0xFFFFFFFFu, e0, s) + (g - __shfl_sync(0xFFFFFFFFu, excl, s));
+      relax_edge(g < total, se, sd, dist, col, w, nk, nv, nrem, cap, ctl, mymin, lane);
+    }
   }
   mymin = __reduce_min_sync(0xFFFFFFFFu, mymin);
   if (lane == 0 && mymin != kInf) atomicMin(&ctl->minkey, mymin);
