@@ -2,7 +2,8 @@
 racecheck, synccheck): KM + kf_meta (m <= 32; ballot / increment / peer-mask
 ranks, producer-warp and per-element stores), KU + KR + kf_fused (m > 32 and
 the single-CTA path), KH + KG + kf_fused (the tile pipeline and the stage API),
-the radix sort, KX (shard merge), kh_histogram; n in {1, 1000, 2^16 (+ ragged)}.
+the radix sort, KX (shard merge), kh_histogram, splitter buckets, the m > 256 path
+(KB / KO / KGA), Multisplit-SSSP; n in {1, 1000, 2^16 (+ ragged)}.
 Each result is compared with the oracle (exit code 1 on a mismatch)."""
 import os
 import sys
@@ -130,6 +131,28 @@ check("hist even", np.array_equal(h(ms.histogram_even(d(x.view(np.uint32)).view(
 check("hist range", np.array_equal(h(ms.histogram_range(d(x.view(np.uint32)).view(torch.float32),
                                                         d(spl.view(np.uint32)).view(torch.float32))),
                                    oracle.histogram_range(x, spl)))
+# splitter buckets (every kernel stages the table), m > 256 (bucket-id pass, two radix
+# passes, offsets, gather), Multisplit-SSSP (splitters + relax)
+for m in (8, 37, 256):
+    spl = np.sort(np.random.default_rng(m).choice(1 << 32, m - 1, replace=False).astype(np.uint64)).astype(np.uint32)
+    for n in (1000, (1 << 16) + 77):
+        k = gen.keys(n, seed=m + 5)
+        v = gen.values(n, seed=3)
+        ek, ev, eo = oracle.multisplit(k, oracle.splitters(spl), v)
+        ko, vo, off = ms.multisplit(d(k), d(v), bucket=ms.Splitters(d(spl)))
+        check(f"splitters m{m} n{n}", np.array_equal(h(ko), ek) and np.array_equal(h(vo), ev) and
+              np.array_equal(h(off), eo))
+for ob, pb in ((oracle.delta(1000), ms.Delta(1000)), (oracle.radix(2, 12), ms.Radix(2, 12))):
+    n = 30011
+    k = gen.keys(n, seed=11)
+    v = gen.values(n, seed=4)
+    ek, ev, eo = oracle.multisplit(k, ob, v)
+    ko, vo, off = ms.multisplit(d(k), d(v), bucket=pb)
+    check(f"large m{ob.m}", np.array_equal(h(ko), ek) and np.array_equal(h(vo), ev) and np.array_equal(h(off), eo))
+from gen.graphs import rmat_csr  # noqa: E402
+V, rp, col, w = rmat_csr(9, 8, seed=2)
+dist = ms.sssp(d(rp), d(col), d(w), 0, delta=50)
+check("sssp", np.array_equal(h(dist), oracle.sssp(rp, col, w, 0)))
 torch.cuda.synchronize()
 print("sanitize cases:", "ok" if bad == 0 else f"{bad} mismatches", flush=True)
 sys.exit(1 if bad else 0)
