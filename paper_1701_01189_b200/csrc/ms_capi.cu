@@ -364,7 +364,8 @@ cudaError_t l0_prescan(const Plan &pl, bool pairs, const uint32_t *keys, uint32_
     return e;
   }
   cudaError_t e = counted(tile_meta_wide(pl, pairs, keys, n, lo.LW, st.KM, st.GM, st.meta, lo.LW, st.R, hdr, s));
-  if (e == cudaSuccess) e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.GM, st.mP, s));
+  if (e == cudaSuccess && with_totals)  // the postscan reduces R itself; KR only for the sharded counts
+    e = counted(launch_level0_scan(st.R, st.P, st.Tot, st.GM, st.mP, s));
   return e;
 }
 
@@ -378,8 +379,8 @@ cudaError_t l0_postscan(const Plan &pl, bool pairs, KfArgs &a, const L0 &st, cud
     a.R = st.R;  // kf_meta reduces the range histograms itself
     return counted(fused_meta(pl, pairs, a, st.G, s));
   }
-  a.R = st.P;
-  a.Tot = st.Tot;
+  a.R = st.R;  // kf_meta_wide reduces the range histograms itself
+  a.r_rows = st.GM;
   a.prefix_step = st.KM == st.K ? 1u : 2u;
   return counted(fused_meta_wide(pl, pairs, a, st.G, s));
 }
@@ -533,6 +534,17 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
                       ms::lane_ordered_inc(false) == 1;
   a.rank_inc = inc_ok && (!pairs || m <= 32);
 
+  if (n <= kSmallMax && ms::lane_ordered_inc(false) == 1 &&
+      g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO) {
+    // latency-bound sizes: one CTA, one pass (k_small, ms_large.cuh)
+    a.mode = kModeSingle;
+    stage_event(0, s);
+    stage_event(1, s);
+    stage_event(2, s);
+    const cudaError_t e = counted(MS_LAUNCH(small, pairs, a, pl.bp, s));
+    stage_event(3, s);
+    return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+  }
   if (n <= lo.T) {  // one subproblem: a single launch
     a.mode = kModeSingle;
     a.num_tiles = 1;

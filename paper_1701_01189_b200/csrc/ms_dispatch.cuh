@@ -59,6 +59,14 @@ struct Launch {
     k_bucket_ids<KIND><<<grid ? grid : 1u, 256, 0, s>>>(keys, n, bp, payload_index ? 1 : 0, b, p, hdr);
     return cudaGetLastError();
   }
+  // n <= kSmallMax in one CTA (ms_large.cuh)
+  static cudaError_t small(bool pairs, const KfArgs &a, const BucketParams &bp, cudaStream_t s) {
+    if (pairs)
+      k_small<KIND, true><<<1, kThreads, 0, s>>>(a, bp);
+    else
+      k_small<KIND, false><<<1, kThreads, 0, s>>>(a, bp);
+    return cudaGetLastError();
+  }
   static cudaError_t merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
                            const BucketParams &bp, const uint32_t *starts, const uint32_t *offs,
                            uint32_t G, uint32_t *keys_out, uint32_t *vals_out, cudaStream_t s);

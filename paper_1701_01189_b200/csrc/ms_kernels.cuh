@@ -247,7 +247,8 @@ struct KfArgs {
   int use_tma;     // TMA bulk loads of input tiles (inputs 16-byte aligned)
   int store_runs;  // TMA bulk stores of whole bucket runs (m <= 64, outputs 16-byte aligned)
   int rank_inc;    // rank by lane-ordered shared-memory increments (reading R23, probed per device)
-  uint32_t prefix_step;  // kf_meta_wide: row of range c in the prefix matrix = c * prefix_step
+  uint32_t prefix_step;  // kf_meta_wide: first row of range c in the range histograms = c * prefix_step
+  uint32_t r_rows;       // kf_meta_wide: rows of the range histograms R (prescan CTAs)
   // sharded fused scatter (KP, Eq.3 with the GPUs as level 0): the bucket bases
   // are the global A_b + B_{b,r} and every element goes to the output window of
   // the rank that owns its global position (kf_meta / kf_meta_wide only)

@@ -11,6 +11,7 @@
 //   KGA k_gather_pairs (pairs only): keys_out[j] = keys[p_j], vals_out[j] = vals[p_j].
 #pragma once
 #include "ms_device.cuh"
+#include "ms_kernels.cuh"
 
 namespace ms {
 
@@ -47,6 +48,89 @@ static __global__ void __launch_bounds__(256)
     const uint32_t i = __ldg(idx + j);
     keys_out[j] = __ldg(keys + i);
     vals_out[j] = __ldg(vals + i);
+  }
+}
+
+}  // namespace ms
+
+namespace ms {
+
+// ============================================================================
+// KT k_small: the whole multisplit of n <= 4096 elements in one CTA of 16
+// warps, for the latency-bound regime (configs[0], n = 2^10; Multisplit-SSSP's
+// small work lists).  Warp w owns elements [256 w, 256 w + 256) as 8
+// windows in input order.  One pass: per-warp ranks by lane-ordered increments
+// (reading R23; only on a device whose probe held), which also leave the
+// (warp, bucket) counts; a column scan over the warps and a scan over the
+// buckets (Eq.2 with the warps as subproblems); every element is then stored
+// at base[b] + (earlier warps' count of b) + rank.  Three barriers, no TMA.
+// ============================================================================
+constexpr uint32_t kSmallMax = 4096;
+
+template <int KIND, bool PAIRS>
+__global__ void __launch_bounds__(kThreads) k_small(KfArgs a, BucketParams bp) {
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
+  constexpr uint32_t W = kWarps, PER = kSmallMax / W, ITEMS = PER / 32;
+  __shared__ uint32_t cnt[W][kMaxBuckets];
+  __shared__ uint32_t s_base[kMaxBuckets];
+  __shared__ uint32_t s_wsum[W];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, m = bp.m;
+  for (uint32_t i = tid; i < W * kMaxBuckets; i += blockDim.x) (&cnt[0][0])[i] = 0u;
+  if (tid == 0) a.hdr[0] = 0u;  // the key-domain flag of this call (set after the barrier)
+  __syncthreads();
+  uint32_t key[ITEMS], b[ITEMS], r[ITEMS], val[PAIRS ? ITEMS : 1];
+  bool derr = false;
+#pragma unroll
+  for (uint32_t i = 0; i < ITEMS; ++i) {
+    const uint32_t e = warp * PER + 32u * i + lane;
+    const bool valid = e < a.n;
+    key[i] = valid ? __ldg(a.keys_in + e) : 0u;
+    if constexpr (PAIRS) val[i] = valid ? __ldg(a.vals_in + e) : 0u;
+    b[i] = bucket_of<KIND>(key[i], bp);
+    if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
+    r[i] = valid ? atomicAdd(&cnt[warp][b[i]], 1u) : 0u;
+  }
+  if constexpr (KIND == kIdentity) {
+    if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
+  }
+  __syncthreads();
+  // column scan over the warps (thread j < m owns bucket j), then the buckets
+  uint32_t tot = 0;
+  if (tid < m) {
+#pragma unroll
+    for (uint32_t w = 0; w < W; ++w) {
+      const uint32_t c = cnt[w][tid];
+      cnt[w][tid] = tot;
+      tot += c;
+    }
+  }
+  uint32_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  if (tid < m) {
+    uint32_t pre = 0;
+    for (uint32_t w = 0; w < warp; ++w) pre += s_wsum[w];
+    const uint32_t base = pre + incl - tot;
+    s_base[tid] = base;
+    if (a.bucket_offsets) {
+      a.bucket_offsets[tid] = base;
+      if (tid == m - 1) a.bucket_offsets[m] = base + tot;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t i = 0; i < ITEMS; ++i) {
+    const uint32_t e = warp * PER + 32u * i + lane;
+    if (e < a.n) {
+      const uint32_t p = s_base[b[i]] + cnt[warp][b[i]] + r[i];
+      a.keys_out[p] = key[i];
+      if constexpr (PAIRS) a.vals_out[p] = val[i];
+    }
   }
 }
 

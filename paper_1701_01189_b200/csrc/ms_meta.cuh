@@ -700,6 +700,15 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
       // ---- next tile's keys into registers before the barrier -----------------
       if (k + 1 < nt) load_tile(tile(k + 1), k + 1);
       named_barrier_sync(1, NT);
+      // ---- refill the stage of tile t-1 with tile t+2 as soon as tile t-1's
+      // bulk stores (issued a whole iteration ago) have read it, before this
+      // tile's stores are queued
+      if (warp == W - 1) {
+        bulk_wait_read();
+        __syncwarp();
+        if (lane == 0) fence_proxy_async_smem();
+        issue(k + 2, (k + 2) % kStages);
+      }
       // ---- run stores of tile t: one TMA bulk store per run body by the last
       // warp, the <= 3 leading / trailing elements by threads 8b .. 8b+7
       if (warp == W - 1) {
@@ -731,14 +740,6 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
           a.keys_out[gs + e] = s_stage[sidx];
           if constexpr (PAIRS) a.vals_out[gs + e] = s_stage[OS + sidx];
         }
-      }
-      // ---- refill the stage of tile t-1 with tile t+2 once its bulk stores
-      // have read it (all groups but the newest)
-      if (warp == W - 1) {
-        bulk_wait_read_newest_pending();
-        __syncwarp();
-        if (lane == 0) fence_proxy_async_smem();
-        issue(k + 2, (k + 2) % kStages);
       }
     } else {
       // ---- next tile's keys into registers before the barrier -----------------

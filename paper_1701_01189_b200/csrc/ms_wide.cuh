@@ -403,13 +403,38 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
   issue_rec(t0, 0);
   issue_rec(t0 + 1, 1);
   for (uint32_t j = 2; j < 2 + kPrefetch; ++j) prefetch(t0 + j, true);
+  // level-0 offsets without a scan kernel: the CTA reduces the range
+  // histograms R (a.r_rows rows of KMW, L2-resident) to the bucket totals and
+  // this range's column prefix (rows < c * prefix_step); stage 2 is scratch
+  // until the first refill
+  {
+    constexpr uint32_t NG = NT / MP;
+    uint32_t *red = stage0 + 2u * SWD;
+    const uint32_t b = tid % MP, g = tid / MP, cp = blockIdx.x * a.prefix_step;
+    uint32_t tp = 0, pp = 0;
+#pragma unroll 8
+    for (uint32_t r = g; r < a.r_rows; r += NG) {
+      const uint32_t x = __ldcg(a.R + (size_t)r * MP + b);
+      tp += x;
+      pp += r < cp ? x : 0u;
+    }
+    red[g * MP + b] = tp;
+    red[(NG + g) * MP + b] = pp;
+  }
+  __syncthreads();
   if (warp == W - 1) {  // the running offsets live in shared memory, kept by the last warp
-    uint32_t grun[NB];
-    const uint32_t c = blockIdx.x;
-    uint32_t tot[NB], s = 0;
+    constexpr uint32_t NG = NT / MP;
+    const uint32_t *red = stage0 + 2u * SWD;
+    uint32_t grun[NB], tot[NB], pre[NB], s = 0;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      tot[j] = __ldcg(a.Tot + lane * NB + j);
+      const uint32_t b = lane * NB + j;
+      tot[j] = pre[j] = 0u;
+#pragma unroll
+      for (uint32_t g = 0; g < NG; ++g) {
+        tot[j] += red[g * MP + b];
+        pre[j] += red[(NG + g) * MP + b];
+      }
       grun[j] = s;
       s += tot[j];
     }
@@ -424,14 +449,14 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
       grun[j] += incl - s;
       const uint32_t b = lane * NB + j;
       if (a.gbase_ovr) grun[j] = b < bp.m ? __ldcg(a.gbase_ovr + b) : 0u;
-      if (c == 0 && a.bucket_offsets) {
+      if (blockIdx.x == 0 && a.bucket_offsets) {
         if (b < bp.m) a.bucket_offsets[b] = grun[j];
         if (b + 1 == bp.m) a.bucket_offsets[bp.m] = grun[j] + tot[j];
       }
-      grun[j] += __ldcg(a.R + (size_t)c * a.prefix_step * MP + b);
-      s_grun[b] = grun[j];
+      s_grun[b] = grun[j] + pre[j];
     }
   }
+  __syncthreads();  // stage 2 scratch read before any refill
   load_tile(t0, 0);
   __syncthreads();  // every warp holds tile t0 in registers before any places into its stage
 
