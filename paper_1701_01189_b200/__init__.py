@@ -35,8 +35,13 @@ class Bucket:
     splitters: torch.Tensor | None = None  # SPLITTERS: m-1 device words
 
     def c(self) -> ms_bucket_fn:
-        sp = self.splitters.data_ptr() if self.splitters is not None and self.splitters.numel() else None
-        return ms_bucket_fn(self.kind, self.m, self.delta, self.shift, self.bits, sp)
+        """The C struct (built once per Bucket: the binding is on the latency path of small calls)."""
+        fn = self.__dict__.get("_c")
+        if fn is None:
+            sp = self.splitters.data_ptr() if self.splitters is not None and self.splitters.numel() else None
+            fn = ms_bucket_fn(self.kind, self.m, self.delta, self.shift, self.bits, sp)
+            self.__dict__["_c"] = fn
+        return fn
 
 
 def Delta(m: int, delta: int | None = None) -> Bucket:
@@ -159,9 +164,11 @@ def multisplit(keys: torch.Tensor, values: torch.Tensor | None = None, bucket: B
     ws = _workspace(workspace, need, dv)
     fn = bucket.c()
     _prepare(keys)
-    with torch.cuda.device(dv):
-        sp = _stream_ptr(stream, dv)
-        _call_multisplit(lib, pairs, keys, values, ko, vo, n, fn, off, ws, sp)
+    if dv.index == torch.cuda.current_device():
+        _call_multisplit(lib, pairs, keys, values, ko, vo, n, fn, off, ws, _stream_ptr(stream, dv))
+    else:
+        with torch.cuda.device(dv):
+            _call_multisplit(lib, pairs, keys, values, ko, vo, n, fn, off, ws, _stream_ptr(stream, dv))
     multisplit.last_workspace = ws
     return ko, vo, off
 
