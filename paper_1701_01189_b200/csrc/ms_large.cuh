@@ -23,7 +23,10 @@ __global__ void __launch_bounds__(256)
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t u = __ldg(keys + i);
     derr |= key_domain_error<KIND>(u, bp);
-    b[i] = bucket_of<KIND>(u, bp);  // SPLITTERS: the table stays in global memory (m-1 > smem)
+    if constexpr (KIND == kSplitters)  // the table stays in global memory (up to 65535 entries)
+      b[i] = splitter_bucket<16>(u, bp);
+    else
+      b[i] = bucket_of<KIND>(u, bp);
     p[i] = payload_index ? i : u;
   }
   if (KIND == kIdentity && __any_sync(0xFFFFFFFFu, derr) && (threadIdx.x & 31u) == 0) atomicOr(hdr, 1u);

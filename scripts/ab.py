@@ -25,17 +25,18 @@ for name, m in cases:
             k, x = kv.split("=")
             ms.set_option(OPT[k], int(x))
         ok = None
-        if run.bucket is not None and wl["n"] <= (1 << 25):
+        if run.bucket is not None and 0 < wl["n"] <= (1 << 25):
             run.step(); torch.cuda.synchronize()
             ob = {"delta": lambda: oracle.delta(m), "identity": lambda: oracle.identity(m),
-                  "radix": lambda: oracle.radix(0, m.bit_length() - 1)}[wl["kind"]]()
+                  "radix": lambda: oracle.radix(0, m.bit_length() - 1),
+                  "splitters": lambda: oracle.splitters(h(run.spl))}[wl["kind"]]()
             ek, ev, eo = oracle.multisplit(h(run.keys), ob, h(run.vals) if run.vals is not None else None)
             ok = bool(np.array_equal(h(run.ko), ek) and np.array_equal(h(run.off), eo) and
                       (run.vals is None or np.array_equal(h(run.vo), ev)))
         times, _, _ = bench.time_steps(run, 20, 3, flush, stage_events=False)
         _, st, _ = bench.time_steps(run, 5, 1, flush, stage_events=True)
         t = sum(times) / len(times)
-        rate = wl["n"] / (t * 1e-3) / 1e9
+        rate = run.n / (t * 1e-3) / (1e6 if wl["unit"] == "MTEPS" else 1e9)
         print(json.dumps({"case": f"{name}:{m}", "var": v or "default", "parity": ok, "rate": round(rate, 2),
                           "frac": round(rate * 1e9 * wl["bpe"] / (hbm * 1e9), 4),
                           "stage_ms": {k: round(x, 4) for k, x in (st or {}).items()}}), flush=True)
