@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
   extern __shared__ __align__(128) uint8_t kfw_raw[];
   __shared__ __align__(8) uint64_t bar[kStages];
   __shared__ uint32_t s_ps[kMaxPeers + 1];  // sharded: output shard starts
+  __shared__ uint32_t s_hot[2];             // per tile parity: the hot bucket, or ~0u
   uint32_t *stage0 = reinterpret_cast<uint32_t *>(kfw_raw);
   uint32_t *s_row = stage0 + kStages * SWD;  // [W][RW] packed running slots
   uint32_t *s_tab = s_row + W * RW;          // [2][MP] global minus tile offsets
@@ -457,7 +458,35 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
     }
   }
   __syncthreads();  // stage 2 scratch read before any refill
+  // a tile whose largest bucket holds more than T/16 elements ranks that bucket
+  // by ballots: lanes of one bucket in one increment instruction serialize in
+  // the shared-memory atomic unit (90 % skew, C3).  The last warp finds it from
+  // the tile's record row 0 (bucket bases) after loading the tile, before the
+  // barrier that precedes the tile's ranking.
+  auto find_hot = [&](uint32_t t, uint32_t k) {
+    const uint32_t *r0 = via_tma(t) ? stage0 + (k % kStages) * SWD + R0 : a.meta + (size_t)t * REC;
+    uint32_t m0[HW], tb[NB];
+    wide_unpack<NB>(via_tma(t) ? reinterpret_cast<const V *>(r0)[lane]
+                               : __ldcg(reinterpret_cast<const V *>(r0) + lane), m0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) tb[j] = (m0[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+    const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, tb[0], 1);
+    uint32_t best = 0, bb = 0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const uint32_t te = j + 1 < NB ? tb[j + 1] : (lane < 31 ? nxt : tile_n(t));
+      if (te - tb[j] > best) {
+        best = te - tb[j];
+        bb = lane * NB + j;
+      }
+    }
+    const uint32_t top = __reduce_max_sync(0xFFFFFFFFu, best);
+    const uint32_t who = __ballot_sync(0xFFFFFFFFu, best == top);
+    const uint32_t hot = __shfl_sync(0xFFFFFFFFu, bb, __ffs(who) - 1);
+    if (lane == 0) s_hot[k & 1u] = top > T / 16u ? hot : ~0u;
+  };
   load_tile(t0, 0);
+  if (warp == W - 1) find_hot(t0, 0);
   __syncthreads();  // every warp holds tile t0 in registers before any places into its stage
 
   uint32_t *brow = s_row + warp * RW;
@@ -497,7 +526,30 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
     // all increments of the warp first, then the placements: the increments
     // are in flight together (the probe checks exactly this back-to-back form)
     bool derr = false;
-    if (tn == T) {
+    const uint32_t hot = s_hot[k & 1u];
+    if (tn == T && hot != ~0u) {
+      // the hot bucket's keys take their slots from one ballot per window
+      // (Alg.3 with the peer mask of a single bucket); the others increment
+      uint32_t hbase = (brow[hot >> 1] >> ((hot & 1u) << 4)) & 0xFFFFu;
+      const uint32_t lt = lanemask_lt();
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) {
+        const uint32_t b = bucket_of<KIND>(key[i], bp);
+        if constexpr (KIND == kIdentity) derr |= key_domain_error<KIND>(key[i], bp);
+        const bool ish = b == hot;
+        const uint32_t hm = __ballot_sync(0xFFFFFFFFu, ish);
+        uint32_t slot;
+        if (ish) {
+          slot = hbase + __popc(hm & lt);
+        } else {
+          slot = atomicAdd(brow + (b >> 1), 1u << ((b & 1u) << 4));
+          slot = (slot >> ((b & 1u) << 4)) & 0xFFFFu;
+        }
+        hbase += __popc(hm);
+        s_stage[slot] = key[i];
+        if constexpr (PAIRS) s_stage[T + slot] = val[i];
+      }
+    } else if (tn == T) {
       uint32_t slot[ITEMS];
 #pragma unroll
       for (int i = 0; i < (int)ITEMS; ++i) {
@@ -530,7 +582,10 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
     if constexpr (KIND == kIdentity) {
       if (__any_sync(0xFFFFFFFFu, derr) && lane == 0) atomicOr(a.hdr, 1u);
     }
-    if (k + 1 < nt) load_tile(t + 1, k + 1);
+    if (k + 1 < nt) {
+      load_tile(t + 1, k + 1);
+      if (warp == W - 1) find_hot(t + 1, k + 1);
+    }
     __syncthreads();
     // ---- refill the stage of tile t-1 with tile t+2: every warp finished tile
     // t-1's scatter before this barrier, so the copy starts a whole scatter
