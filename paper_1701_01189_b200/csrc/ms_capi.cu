@@ -396,9 +396,9 @@ struct LargeLayout {
 };
 LargeLayout large_layout(uint64_t n, uint32_t kind, bool pairs) {
   LargeLayout lo{};
-  const bool radix = kind == MS_BUCKET_RADIX;
+  const bool radix = kind == MS_BUCKET_RADIX;  // (top-bit DELTA uses the DELTA layout: a superset)
   lo.inner = kHdrBytes;
-  lo.inner_bytes = ms_multisplit_workspace_size(n, 256, radix ? pairs : true);
+  lo.inner_bytes = std::max(ms_multisplit_workspace_size(n, 256, 0), ms_multisplit_workspace_size(n, 256, 1));
   size_t off = lo.inner + align_up(lo.inner_bytes);
   const int arrays = radix ? (pairs ? 2 : 1) : (pairs ? 6 : 5);
   for (int i = 0; i < arrays; ++i) {
@@ -432,10 +432,16 @@ ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
   uint32_t *hdr = (uint32_t *)w;
   ev(0);
   if (cudaMemsetAsync(hdr, 0, 8, s) != cudaSuccess) return done(MS_ERR_CUDA);
-  if (fn->kind == MS_BUCKET_RADIX) {
+  // RADIX digits, and DELTA buckets that are the top bits of the key (Delta a
+  // power of two with m * Delta >= 2^32: f(u) = u >> s), are radix passes over
+  // the keys themselves: no bucket-id pass, no gather
+  const Plan tp = make_plan(fn);
+  const bool top = tp.kind == kTopBits;
+  if (fn->kind == MS_BUCKET_RADIX || top) {
+    const uint32_t sh = top ? tp.bp.shift : fn->shift, bits = top ? 32u - tp.bp.shift : fn->bits;
     uint32_t *tk = (uint32_t *)(w + lo.x[0]), *tv = pairs ? (uint32_t *)(w + lo.x[1]) : nullptr;
-    const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, fn->shift, 8u, nullptr};
-    const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (fn->bits - 8u), 0u, fn->shift + 8u, fn->bits - 8u, nullptr};
+    const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, sh, 8u, nullptr};
+    const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (bits - 8u), 0u, sh + 8u, bits - 8u, nullptr};
     ev(1);
     ms_status st = multisplit_impl(keys_in, vals_in, tk, tv, n, &a, nullptr, inner, lo.inner_bytes, s, pairs);
     if (st != MS_SUCCESS) return done(st);
@@ -444,7 +450,7 @@ ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
     if (st != MS_SUCCESS) return done(st);
     if (bucket_offsets) {
       k_offsets_sorted<<<min((uint32_t)((n + 256u) / 256u), 148u * 8u), 256, 0, s>>>(
-          keys_out, (uint32_t)n, fn->shift, m - 1u, m, bucket_offsets);
+          keys_out, (uint32_t)n, sh, (uint32_t)((1ull << bits) - 1u), m, bucket_offsets);
       if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
     }
     ev(3);
