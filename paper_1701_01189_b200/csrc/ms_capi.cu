@@ -396,7 +396,8 @@ struct LargeLayout {
 };
 LargeLayout large_layout(uint64_t n, uint32_t kind, bool pairs) {
   LargeLayout lo{};
-  const bool radix = kind == MS_BUCKET_RADIX;  // (top-bit DELTA uses the DELTA layout: a superset)
+  // RADIX and IDENTITY: two key passes (top-bit DELTA uses the DELTA layout, a superset)
+  const bool radix = kind == MS_BUCKET_RADIX || kind == MS_BUCKET_IDENTITY;
   lo.inner = kHdrBytes;
   lo.inner_bytes = std::max(ms_multisplit_workspace_size(n, 256, 0), ms_multisplit_workspace_size(n, 256, 1));
   size_t off = lo.inner + align_up(lo.inner_bytes);
@@ -435,10 +436,19 @@ ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
   // RADIX digits, and DELTA buckets that are the top bits of the key (Delta a
   // power of two with m * Delta >= 2^32: f(u) = u >> s), are radix passes over
   // the keys themselves: no bucket-id pass, no gather
+  // Identity buckets are the key's low bits (keys >= m are domain errors,
+  // flagged by one check pass; their output is unspecified but in bounds).
   const Plan tp = make_plan(fn);
-  const bool top = tp.kind == kTopBits;
-  if (fn->kind == MS_BUCKET_RADIX || top) {
-    const uint32_t sh = top ? tp.bp.shift : fn->shift, bits = top ? 32u - tp.bp.shift : fn->bits;
+  const bool top = tp.kind == kTopBits, ident = fn->kind == MS_BUCKET_IDENTITY;
+  if (fn->kind == MS_BUCKET_RADIX || top || ident) {
+    uint32_t hb = 0;
+    while ((1u << hb) < m) ++hb;
+    const uint32_t sh = top ? tp.bp.shift : (ident ? 0u : fn->shift);
+    const uint32_t bits = top ? 32u - tp.bp.shift : (ident ? hb : fn->bits);
+    if (ident) {
+      k_domain_check<<<min((uint32_t)((n + 255u) / 256u), 148u * 8u), 256, 0, s>>>(keys_in, (uint32_t)n, m, hdr);
+      if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
+    }
     uint32_t *tk = (uint32_t *)(w + lo.x[0]), *tv = pairs ? (uint32_t *)(w + lo.x[1]) : nullptr;
     const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, sh, 8u, nullptr};
     const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (bits - 8u), 0u, sh + 8u, bits - 8u, nullptr};

@@ -32,6 +32,16 @@ __global__ void __launch_bounds__(256)
   if (KIND == kIdentity && __any_sync(0xFFFFFFFFu, derr) && (threadIdx.x & 31u) == 0) atomicOr(hdr, 1u);
 }
 
+// identity buckets with m > 256 run as radix passes over the keys: the
+// key-domain check (u < m, reading R8) is this separate read
+static __global__ void __launch_bounds__(256)
+    k_domain_check(const uint32_t *__restrict__ keys, uint32_t n, uint32_t m, uint32_t *__restrict__ hdr) {
+  bool bad = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    bad |= __ldg(keys + i) >= m;
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31u) == 0) atomicOr(hdr, 1u);
+}
+
 // src sorted by d(x) = (x >> shift) & mask: off[j] = first index with d >= j, off[m] = n.
 static __global__ void __launch_bounds__(256)
     k_offsets_sorted(const uint32_t *__restrict__ src, uint32_t n, uint32_t shift, uint32_t mask,
