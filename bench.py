@@ -540,7 +540,9 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": metric_name(wl, args.workload, m),
         "value": round(value, 3), "unit": wl["unit"], "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "ms_per_step_median": round(statistics.median(times), 5), "ms_per_step_min": round(min(times), 5),
+        "higher_is_better": True,
         "scaling": "strong" if wl.get("strong") else "weak", "vs_baseline": None, "dtype": "f32" if wl["kind"].startswith("hist") else "u32",
         "data": "synthetic (seeded counter-based generator)",
         "config": {"workload": wl["desc"], "n_per_rank": n, "n_total": n * world, "m": m, "bucket": wl["kind"],

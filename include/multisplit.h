@@ -322,6 +322,13 @@ typedef struct ms_comm ms_comm;
 ms_status ms_comm_unique_id(void *out128);
 ms_status ms_comm_init(ms_comm **comm, int nranks, int rank, const void *id128, int cuda_device);
 ms_status ms_comm_destroy(ms_comm *comm);
+/* Failure detection: ms_comm_check returns MS_ERR_NCCL if the
+ * communicator reported an asynchronous error (ncclCommGetAsyncError), e.g. a
+ * peer that died; ms_comm_abort then aborts the NCCL communicator
+ * (ncclCommAbort) so that no collective blocks forever -- the caller still
+ * calls ms_comm_destroy.  Both are host-only and do not synchronize. */
+ms_status ms_comm_check(ms_comm *comm);
+ms_status ms_comm_abort(ms_comm *comm);
 ms_status ms_comm_register_output(ms_comm *comm, uint32_t *keys_out, uint32_t *vals_out,
                                   uint64_t n_local);
 size_t ms_sharded_workspace_size(const ms_comm *comm, uint64_t n_local, uint32_t m, int with_values);

@@ -79,6 +79,8 @@ SIGNATURES = [
     ("ms_comm_unique_id", _I, [_P]),
     ("ms_comm_init", _I, [ctypes.POINTER(ctypes.c_void_p), _I, _I, _P, _I]),
     ("ms_comm_destroy", _I, [_P]),
+    ("ms_comm_check", _I, [_P]),
+    ("ms_comm_abort", _I, [_P]),
     ("ms_comm_register_output", _I, [_P, _P, _P, _U64]),
     ("ms_sharded_workspace_size", _SZ, [_P, _U64, _U32, _I]),
     ("ms_multisplit_keys_sharded", _I, [_P, _P, _P, _U64, _FN, _P, _P, _SZ, _P]),

@@ -1353,6 +1353,26 @@ ms_status ms_comm_init(ms_comm **out, int nranks, int rank, const void *id128, i
   return MS_SUCCESS;
 }
 
+ms_status ms_comm_check(ms_comm *c) {
+  if (!c) return MS_ERR_INVALID_VALUE;
+  const NcclApi &nc = nccl();
+  if (!nc.ok || !c->nccl) return MS_ERR_NCCL;
+  if (!nc.CommGetAsyncError) return MS_SUCCESS;
+  ncclResult_t r = ncclSuccess;
+  if (nc.CommGetAsyncError(c->nccl, &r) != ncclSuccess) return MS_ERR_NCCL;
+  return (r == ncclSuccess || r == ncclInProgress) ? MS_SUCCESS : MS_ERR_NCCL;
+}
+
+ms_status ms_comm_abort(ms_comm *c) {
+  if (!c) return MS_ERR_INVALID_VALUE;
+  const NcclApi &nc = nccl();
+  if (c->nccl && nc.CommAbort) {
+    nc.CommAbort(c->nccl);
+    c->nccl = nullptr;  // ms_comm_destroy still releases the rest
+  }
+  return MS_SUCCESS;
+}
+
 ms_status ms_comm_destroy(ms_comm *c) {
   if (!c) return MS_ERR_INVALID_VALUE;
   for (int i = 0; i < c->nopened; ++i) cudaIpcCloseMemHandle(c->opened[i]);

@@ -25,6 +25,9 @@ struct NcclApi {
   ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  // failure detection (optional symbols: checked where used)
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 inline const NcclApi &nccl() {
@@ -45,6 +48,8 @@ inline const NcclApi &nccl() {
     MS_NCCL_SYM(Recv);
     MS_NCCL_SYM(GroupStart);
     MS_NCCL_SYM(GroupEnd);
+    MS_NCCL_SYM(CommGetAsyncError);
+    MS_NCCL_SYM(CommAbort);
 #undef MS_NCCL_SYM
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
              api.AllReduce && api.Send && api.Recv && api.GroupStart && api.GroupEnd;

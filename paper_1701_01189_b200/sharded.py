@@ -62,6 +62,14 @@ class Comm:
     def workspace_size(self, n_local: int, m: int, with_values: bool) -> int:
         return int(_lib.load().ms_sharded_workspace_size(self._c, n_local, m, int(with_values)))
 
+    def check(self) -> None:
+        """ms_comm_check: raise MultisplitError(MS_ERR_NCCL) if NCCL reported an async error."""
+        check(_lib.load().ms_comm_check(self._c), "ms_comm_check")
+
+    def abort(self) -> None:
+        """ms_comm_abort: abort the NCCL communicator after a failure (then close())."""
+        check(_lib.load().ms_comm_abort(self._c), "ms_comm_abort")
+
     def close(self) -> None:
         if self._c:
             check(_lib.load().ms_comm_destroy(self._c), "ms_comm_destroy")

@@ -115,6 +115,24 @@ def test_sharded_call_world1(comm1, m, pairs, registered):
     assert goff.cpu().numpy().tolist() == eo.astype(np.int64).tolist()
 
 
+def test_comm_failure_detection_world1():
+    """ms_comm_check on a healthy communicator, then ms_comm_abort + close (a fresh comm:
+    the module fixture keeps its own)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        c = sharded.Comm()
+        c.check()
+        c.abort()
+        c.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
+
+
 def run_merge_virtual(keys_np, vals_np, sizes, bucket):
     """The NCCL path's plan + KX merge with the send/receive done by slicing."""
     G = len(sizes)
