@@ -209,7 +209,7 @@ static cudaError_t kmw_go(const uint32_t *keys, uint32_t n, uint32_t num_tiles, 
   static std::atomic<unsigned long long> done{0};
   const cudaError_t e = set_max_smem(kern, kmw_smem_bytes(NB, PAIRS), done);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads + 32, kmw_smem_bytes(NB, PAIRS), s>>>(keys, n, num_tiles, per, bp, meta,
+  kern<<<grid, kThreads + 32 * kmw_scan_warps(NB), kmw_smem_bytes(NB, PAIRS), s>>>(keys, n, num_tiles, per, bp, meta,
                                                                        nkf, R, hdr);
   return cudaGetLastError();
 }

@@ -149,8 +149,13 @@ __device__ __forceinline__ typename WideVec<NB>::T wide_pack(const uint32_t (&w)
 // ============================================================================
 __host__ __device__ constexpr uint32_t kmw_unit() { return 8192u; }
 
+// Scan warps: two at m > 128 (each owns half the buckets; the one scan warp
+// was the prescan's bottleneck there, measured: the counting warps waited on
+// the counter buffer for 60 % of their samples), else one.
+__host__ __device__ constexpr uint32_t kmw_scan_warps(uint32_t nb) { return nb == 8 ? 2u : 1u; }
+
 template <int KIND, int NB, bool PAIRS>
-__global__ void __launch_bounds__(kThreads + 32, 2)
+__global__ void __launch_bounds__(kThreads + 64, 2)
     km_meta_wide(const uint32_t *__restrict__ keys, uint32_t n, uint32_t num_tiles,
                  uint32_t tiles_per_cta, BucketParams bp, uint32_t *__restrict__ meta,
                  uint32_t num_kf_tiles, uint32_t *__restrict__ R, uint32_t *__restrict__ hdr) {
@@ -159,15 +164,18 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
   constexpr uint32_t H = W / CW;                  // TMA units per tile
   constexpr uint32_t KS = kmw_stages(NB, PAIRS);  // units in the ring
   constexpr uint32_t CB = kmw_cnt_bufs(NB, PAIRS);  // counter buffers
-  constexpr uint32_t HW = NB / 2;                 // packed record words per lane per row
+  constexpr uint32_t SW = kmw_scan_warps(NB);     // scan warps
+  constexpr int LB = NB / SW;                     // buckets per scan lane
+  constexpr uint32_t HL = LB / 2;                 // packed record words per scan lane per row
   constexpr uint32_t RW = 16u * NB;               // packed record words per row (mP / 2)
   constexpr uint32_t MP = 32u * NB;               // counters per row
   constexpr uint32_t REC = wide_rec_words(PAIRS, NB);
-  using V = typename WideVec<NB>::T;
-  extern __shared__ __align__(128) uint32_t kmw_smem[];  // stages [KS][U] | cnt[2][W][MP]
+  using VL = typename WideVec<LB>::T;
+  extern __shared__ __align__(128) uint32_t kmw_smem[];  // stages [KS][U] | cnt[CB][W][MP]
   __shared__ __align__(8) uint64_t full[KS];
   __shared__ __align__(8) uint64_t sfree[KS];
   __shared__ __align__(8) uint64_t cempty[2];
+  __shared__ uint32_t s_carry[2];  // SW = 2: the first scan warp's bucket total, by tile parity
   griddep_launch_dependents();
   uint32_t *cnt = kmw_smem + KS * U;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -184,23 +192,24 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
       mbar_init(&full[i], 1);
       mbar_init(&sfree[i], CW * 32u);
     }
-    for (uint32_t i = 0; i < 2; ++i) mbar_init(&cempty[i], 32);
+    for (uint32_t i = 0; i < 2; ++i) mbar_init(&cempty[i], 32u * SW);
   }
   __syncthreads();
 
-  if (warp == CW) {
-    // ============================ scan warp ===================================
+  if (warp >= CW) {
+    // ============================ scan warps ==================================
+    const uint32_t sidx = warp - CW, blk = sidx * 32u + lane;  // this lane's bucket block
     auto issue = [&](uint32_t u) {
-      if (lane == 0 && u < nu && via_tma(u)) {
+      if (sidx == 0 && lane == 0 && u < nu && via_tma(u)) {
         const uint32_t st = u % KS;
         mbar_arrive_expect_tx(&full[st], U * 4u);
         tma_load_1d(kmw_smem + st * U, keys + unit_start(u), U * 4u, &full[st], policy_evict_first());
       }
     };
     for (uint32_t u = 0; u < KS; ++u) issue(u);
-    uint32_t running[NB];
+    uint32_t running[LB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) running[j] = 0u;
+    for (int j = 0; j < LB; ++j) running[j] = 0u;
     uint32_t k = 0;
     for (uint32_t t = t0; t < t1; ++t, ++k) {
       const uint32_t p = k % CB;
@@ -213,20 +222,21 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
       }
       uint32_t *c = cnt + p * W * MP;
       // pass 1: tile count h of this lane's buckets
-      uint32_t hc[NB];
+      uint32_t hc[LB];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) hc[j] = 0u;
+      for (int j = 0; j < LB; ++j) hc[j] = 0u;
 #pragma unroll 4
       for (uint32_t w = 0; w < W; ++w) {
-        uint32_t x[NB];
-        ld_words<NB>(c + w * MP + lane * NB, x);
+        uint32_t x[LB];
+        ld_words<LB>(c + w * MP + blk * LB, x);
 #pragma unroll
-        for (int j = 0; j < NB; ++j) hc[j] += x[j];
+        for (int j = 0; j < LB; ++j) hc[j] += x[j];
       }
-      // exclusive scan over the buckets (in-lane prefix + warp scan of lane sums)
-      uint32_t tb[NB], s = 0;
+      // exclusive scan over the buckets (in-lane prefix, warp scan of lane sums,
+      // and the first scan warp's total for the second)
+      uint32_t tb[LB], s = 0;
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
+      for (int j = 0; j < LB; ++j) {
         tb[j] = s;
         s += hc[j];
       }
@@ -236,33 +246,39 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
         const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= (uint32_t)o) incl += y;
       }
+      uint32_t carry = 0;
+      if constexpr (SW == 2) {
+        if (sidx == 0 && lane == 31) s_carry[k & 1u] = incl;
+        named_barrier_sync(1, 64);
+        if (sidx == 1) carry = s_carry[k & 1u];
+      }
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        tb[j] += incl - s;
+      for (int j = 0; j < LB; ++j) {
+        tb[j] += incl - s + carry;
         running[j] += hc[j];
       }
       // pass 2: S[w][b] = tb[b] + sum_{w'<w} c_{w',b} (16-bit); zero the counters
       uint32_t *rec = meta + (size_t)t * REC;
 #pragma unroll 2
       for (uint32_t w = 0; w < W; ++w) {
-        uint32_t *cw = c + w * MP + lane * NB;
-        uint32_t x[NB], o[HW];
-        ld_words<NB>(cw, x);
+        uint32_t *cw = c + w * MP + blk * LB;
+        uint32_t x[LB], o[HL];
+        ld_words<LB>(cw, x);
 #pragma unroll
-        for (int i = 0; i < (int)HW; ++i) {
+        for (int i = 0; i < (int)HL; ++i) {
           o[i] = (tb[2 * i] & 0xFFFFu) | (tb[2 * i + 1] << 16);
           tb[2 * i] += x[2 * i];
           tb[2 * i + 1] += x[2 * i + 1];
         }
-        st_zero_words<NB>(cw);
-        if (t < num_kf_tiles) reinterpret_cast<V *>(rec + w * RW)[lane] = wide_pack<NB>(o);
+        st_zero_words<LB>(cw);
+        if (t < num_kf_tiles) reinterpret_cast<VL *>(rec + w * RW)[blk] = wide_pack<LB>(o);
       }
       __syncwarp();
       mbar_arrive(&cempty[p]);
     }
-    uint32_t *r = R + (size_t)blockIdx.x * (32u * NB) + lane * NB;
+    uint32_t *r = R + (size_t)blockIdx.x * MP + blk * LB;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) r[j] = running[j];
+    for (int j = 0; j < LB; ++j) r[j] = running[j];
     return;
   }
 
