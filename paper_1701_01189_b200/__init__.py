@@ -198,7 +198,7 @@ def radix_sort(keys: torch.Tensor, values: torch.Tensor | None = None, *, begin_
                out_values: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                stream=None):
     """LSD multisplit radix sort (Sec.7.1): stable sort by key bits [begin_bit, end_bit).
-    bits_per_pass = 0: the library's choice (5-bit digits, see include/multisplit.h)."""
+    bits_per_pass = 0: the library's choice (8-bit digits, see include/multisplit.h)."""
     lib = _lib.load()
     keys = _u32view(keys, "keys")
     dv = keys.device

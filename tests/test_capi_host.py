@@ -52,10 +52,10 @@ def test_radix_schedule_golden(lib):
     assert lib.ms_radix_pass_schedule(0, 32, 9, None, None, 0) == -1
     assert lib.ms_radix_pass_schedule(8, 8, 4, None, None, 0) == -1
     assert lib.ms_radix_pass_schedule(4, 20, 8, None, None, 0) == 2
-    # bits_per_pass = 0: the library's choice, 5-bit digits (six of 5 bits + one of 2)
+    # bits_per_pass = 0: the library's choice, 8-bit digits (four passes)
     import paper_1701_01189_b200 as ms
-    assert ms.radix_pass_schedule(0, 32, 0) == ms.radix_pass_schedule(0, 32, 5)
-    assert [b for _, b in ms.radix_pass_schedule(0, 32, 0)] == [5, 5, 5, 5, 5, 5, 2]
+    assert ms.radix_pass_schedule(0, 32, 0) == ms.radix_pass_schedule(0, 32, 8)
+    assert [b for _, b in ms.radix_pass_schedule(0, 32, 0)] == [8, 8, 8, 8]
 
 
 def test_bucket_helpers(lib):

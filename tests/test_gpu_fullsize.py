@@ -58,9 +58,9 @@ def test_c3_pairs_2p27(m, kind, dist):
     assert np.array_equal(host(ko), ek) and np.array_equal(host(vo), ev) and np.array_equal(host(off), eo)
 
 
-@pytest.mark.parametrize("r", [8, 0])
+@pytest.mark.parametrize("r", [8, 5])
 def test_c4_radix_sort_pairs_2p28(r):
-    """configs[3] as benched (r = 8: 4 x 8-bit passes over [0, 32)) and the library default."""
+    """configs[3] as benched (r = 8: 4 x 8-bit passes over [0, 32), also the library default) and 5-bit digits."""
     n = 1 << 28
     k, v = gen_dev(n, 0x5EED)
     ko, vo = ms.radix_sort(k, v, begin_bit=0, end_bit=32, bits_per_pass=r)
