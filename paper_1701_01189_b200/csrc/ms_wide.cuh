@@ -506,6 +506,15 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
   __syncthreads();  // every warp holds tile t0 in registers before any places into its stage
 
   uint32_t *brow = s_row + warp * RW;
+  // placement into the stage: keys alone, or (key, value) as one 64-bit word
+  // (pairs: one store here and one load in the scatter instead of two each;
+  // the stage's raw data is dead once every warp holds the tile in registers)
+  auto place = [&](uint32_t *st, uint32_t slot, uint32_t k_, uint32_t v_) {
+    if constexpr (PAIRS)
+      reinterpret_cast<uint2 *>(st)[slot] = make_uint2(k_, v_);
+    else
+      st[slot] = k_;
+  };
   for (uint32_t k = 0; k < nt; ++k) {
     const uint32_t t = t0 + k;
     const uint32_t st = k % kStages;
@@ -562,8 +571,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
           slot = (slot >> ((b & 1u) << 4)) & 0xFFFFu;
         }
         hbase += __popc(hm);
-        s_stage[slot] = key[i];
-        if constexpr (PAIRS) s_stage[T + slot] = val[i];
+        place(s_stage, slot, key[i], PAIRS ? val[i] : 0u);
       }
     } else if (tn == T) {
       uint32_t slot[ITEMS];
@@ -575,11 +583,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
         slot[i] = (slot[i] >> ((b & 1u) << 4)) & 0xFFFFu;
       }
 #pragma unroll
-      for (int i = 0; i < (int)ITEMS; ++i) s_stage[slot[i]] = key[i];
-      if constexpr (PAIRS) {
-#pragma unroll
-        for (int i = 0; i < (int)ITEMS; ++i) s_stage[T + slot[i]] = val[i];
-      }
+      for (int i = 0; i < (int)ITEMS; ++i) place(s_stage, slot[i], key[i], PAIRS ? val[i] : 0u);
     } else {
 #pragma unroll
       for (int i = 0; i < (int)ITEMS; ++i) {
@@ -590,8 +594,7 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
         if (valid) {
           const uint32_t sh = (b & 1u) << 4;
           const uint32_t slot = (atomicAdd(brow + (b >> 1), 1u << sh) >> sh) & 0xFFFFu;
-          s_stage[slot] = key[i];
-          if constexpr (PAIRS) s_stage[T + slot] = val[i];
+          place(s_stage, slot, key[i], PAIRS ? val[i] : 0u);
         }
       }
     }
@@ -619,16 +622,23 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
       constexpr uint32_t CH = 8;
 #pragma unroll
       for (uint32_t c = 0; c < ITEMS; c += CH) {
-        uint32_t kk[CH], pos[CH];
+        uint32_t kk[CH], vv[PAIRS ? CH : 1], pos[CH];
 #pragma unroll
-        for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[s0 + 32 * (c + i)];
+        for (uint32_t i = 0; i < CH; ++i) {
+          if constexpr (PAIRS) {
+            const uint2 kv = reinterpret_cast<const uint2 *>(s_stage)[s0 + 32 * (c + i)];
+            kk[i] = kv.x;
+            vv[i] = kv.y;
+          } else {
+            kk[i] = s_stage[s0 + 32 * (c + i)];
+          }
+        }
 #pragma unroll
         for (uint32_t i = 0; i < CH; ++i) pos[i] = tab[bucket_of<KIND>(kk[i], bp)] + s0 + 32 * (c + i);
         if (a.npeers) {  // sharded: into the owning rank's window (KP)
 #pragma unroll
           for (uint32_t i = 0; i < CH; ++i)
-            if (s0 + 32 * (c + i) < tn)
-              kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? s_stage[T + s0 + 32 * (c + i)] : 0u);
+            if (s0 + 32 * (c + i) < tn) kp_store<PAIRS>(a, s_ps, pos[i], kk[i], PAIRS ? vv[i] : 0u);
         } else if (tn == T) {  // full tile: no per-element predicates
           uint32_t *__restrict__ ko = a.keys_out;
 #pragma unroll
@@ -636,21 +646,15 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
           if constexpr (PAIRS) {
             uint32_t *__restrict__ vo = a.vals_out;
 #pragma unroll
-            for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[T + s0 + 32 * (c + i)];
-#pragma unroll
-            for (uint32_t i = 0; i < CH; ++i) vo[pos[i]] = kk[i];
+            for (uint32_t i = 0; i < CH; ++i) vo[pos[i]] = vv[i];
           }
         } else {
 #pragma unroll
           for (uint32_t i = 0; i < CH; ++i)
-            if (s0 + 32 * (c + i) < tn) a.keys_out[pos[i]] = kk[i];
-          if constexpr (PAIRS) {
-#pragma unroll
-            for (uint32_t i = 0; i < CH; ++i) kk[i] = s_stage[T + s0 + 32 * (c + i)];
-#pragma unroll
-            for (uint32_t i = 0; i < CH; ++i)
-              if (s0 + 32 * (c + i) < tn) a.vals_out[pos[i]] = kk[i];
-          }
+            if (s0 + 32 * (c + i) < tn) {
+              a.keys_out[pos[i]] = kk[i];
+              if constexpr (PAIRS) a.vals_out[pos[i]] = vv[i];
+            }
         }
       }
     }
