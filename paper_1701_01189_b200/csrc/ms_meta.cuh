@@ -151,14 +151,20 @@ __global__ void __launch_bounds__(kThreads + 32, 2)
       uint4 q[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) q[u] = v[lane + 32u * (uint32_t)u];
+      // every bucket id first, then the increments: the compiler cannot move a
+      // shared-memory load (the splitter search) above an atomic on the
+      // counters, so interleaving them serialized the searches
+      uint32_t bk[4 * NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
-        const uint32_t k4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+        bk[4 * u] = bucket_of<KIND>(q[u].x, bp);
+        bk[4 * u + 1] = bucket_of<KIND>(q[u].y, bp);
+        bk[4 * u + 2] = bucket_of<KIND>(q[u].z, bp);
+        bk[4 * u + 3] = bucket_of<KIND>(q[u].w, bp);
+      }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t b = bucket_of<KIND>(k4[e], bp);
-          if constexpr (SMALLM) ones += b; else atomicAdd(row + b, 1u);
-        }
+      for (int e = 0; e < 4 * NV; ++e) {
+        if constexpr (SMALLM) ones += bk[e]; else atomicAdd(row + bk[e], 1u);
       }
     } else {  // ragged last tile / unaligned input
       const uint64_t lo = (uint64_t)t * T + warp * SL;
@@ -570,11 +576,14 @@ __global__ void __launch_bounds__(PROD ? kThreads + 32 : kThreads, 2) kf_meta(Kf
         __syncwarp();
         // (one increment, then its placement: issuing all increments first was
         // measured slower at m = 8 / 16, where more lanes share a counter)
+        uint32_t bk[ITEMS];  // bucket ids first (see KM): the searches interleave
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) bk[i] = bucket_of<KIND>(key[i], bp);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
           const bool valid = FULL || wbase + (uint32_t)i * 32u + lane < tn;
           if (!FULL && wbase + (uint32_t)i * 32u >= tn) continue;
-          const uint32_t b = bucket_of<KIND>(key[i], bp);
+          const uint32_t b = bk[i];
           if constexpr (KIND == kIdentity) derr |= valid && key_domain_error<KIND>(key[i], bp);
           if (valid) {
             const uint32_t slot = atomicAdd(brow + b, 1u);

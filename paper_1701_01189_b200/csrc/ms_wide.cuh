@@ -293,14 +293,16 @@ __global__ void __launch_bounds__(kThreads + 64, 2)
       uint4 q[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) q[i] = v[lane + 32u * (uint32_t)i];
+      uint32_t bk[16];  // bucket ids first, then the increments (see km_tile_meta)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint32_t k4[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          atomicAdd(row + bucket_of<KIND>(k4[e], bp), 1u);
-        }
+        bk[4 * i] = bucket_of<KIND>(q[i].x, bp);
+        bk[4 * i + 1] = bucket_of<KIND>(q[i].y, bp);
+        bk[4 * i + 2] = bucket_of<KIND>(q[i].z, bp);
+        bk[4 * i + 3] = bucket_of<KIND>(q[i].w, bp);
       }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) atomicAdd(row + bk[e], 1u);
     } else {  // ragged last unit / unaligned input
       const uint64_t lo = unit_start(u) + warp * SL;
       const uint32_t hi = (uint32_t)min((uint64_t)n, lo + SL);
@@ -574,10 +576,12 @@ __global__ void __launch_bounds__(wide_kw(PAIRS) * 32, wide_ctas_per_sm(PAIRS)) 
         place(s_stage, slot, key[i], PAIRS ? val[i] : 0u);
       }
     } else if (tn == T) {
-      uint32_t slot[ITEMS];
+      uint32_t slot[ITEMS], bk[ITEMS];
+#pragma unroll
+      for (int i = 0; i < (int)ITEMS; ++i) bk[i] = bucket_of<KIND>(key[i], bp);  // searches interleave
 #pragma unroll
       for (int i = 0; i < (int)ITEMS; ++i) {
-        const uint32_t b = bucket_of<KIND>(key[i], bp);
+        const uint32_t b = bk[i];
         if constexpr (KIND == kIdentity) derr |= key_domain_error<KIND>(key[i], bp);
         slot[i] = atomicAdd(brow + (b >> 1), 1u << ((b & 1u) << 4));
         slot[i] = (slot[i] >> ((b & 1u) << 4)) & 0xFFFFu;
