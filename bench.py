@@ -61,10 +61,26 @@ WORKLOADS = {
     "ms_sharded_c5": dict(n=1 << 30, pairs=True, kind="delta", m=256, unit="Gpairs/s", bpe=20,
                           desc="sharded key-value multisplit, n=2^30 pairs in total over the ranks, m=256 "
                                "delta buckets (configs[4]); n is per job, split evenly", strong=True),
-    "sort_keys": dict(n=1 << 28, pairs=False, kind="sort", m=256, unit="Gkeys/s", bpe=48,
+    # the sorts' default path is the one-pass pipeline (f1): every digit histogram in
+    # one read, then one fused look-back pass per digit (bpe_f1 = 36 / 68 B); bpe
+    # stays the paper-faithful accounting (each pass a full multisplit, 48 / 80 B)
+    "sort_keys": dict(n=1 << 28, pairs=False, kind="sort", m=256, unit="Gkeys/s", bpe=48, bpe_f1=36,
                       desc="multisplit LSD radix sort, 2^28 uint32 keys, 4 x 8-bit (configs[3])"),
-    "sort_pairs": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80,
+    "sort_pairs": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80, bpe_f1=68,
                        desc="multisplit LSD radix sort, 2^28 pairs, 4 x 8-bit (configs[3])"),
+    "sort_keys_passes": dict(n=1 << 28, pairs=False, kind="sort", m=256, unit="Gkeys/s", bpe=48,
+                             opts={"MS_OPT_SORT": "MS_SORT_PASSES"},
+                             desc="multisplit LSD radix sort, 2^28 keys, 4 x 8-bit, each pass a full multisplit"),
+    "sort_pairs_passes": dict(n=1 << 28, pairs=True, kind="sort", m=256, unit="Gpairs/s", bpe=80,
+                              opts={"MS_OPT_SORT": "MS_SORT_PASSES"},
+                              desc="multisplit LSD radix sort, 2^28 pairs, 4 x 8-bit, each pass a full multisplit"),
+    # the one-pass multisplit (f1, MS_PIPELINE_ONESWEEP): bucket counts + one fused kernel
+    "ms_keys_os": dict(n=1 << 25, pairs=False, kind="delta", m=32, unit="Gkeys/s", bpe=12,
+                       opts={"MS_OPT_PIPELINE": "MS_PIPELINE_ONESWEEP"},
+                       desc="key-only multisplit, n=2^25, delta buckets, one-pass pipeline (f1)"),
+    "ms_pairs_os": dict(n=1 << 25, pairs=True, kind="delta", m=32, unit="Gpairs/s", bpe=20,
+                        opts={"MS_OPT_PIPELINE": "MS_PIPELINE_ONESWEEP"},
+                        desc="key-value multisplit, n=2^25, delta buckets, one-pass pipeline (f1)"),
     # the same sorts with 5-bit digits: 7 passes through the m <= 32 pipeline
     # (the paper's Table 8 sweeps r); bpe counts the 7 passes
     "sort_keys_r5": dict(n=1 << 28, pairs=False, kind="sort", m=32, bits=5, unit="Gkeys/s", bpe=84,
@@ -263,6 +279,20 @@ class Runner:
         return st
 
     def step(self, keys=None, ko=None):
+        opts = self.wl.get("opts")
+        if not opts:
+            return self._step(keys, ko)
+        lib = self.ms._lib
+        saved = {o: self.ms.get_option(getattr(lib, o)) for o in opts}
+        for o, v in opts.items():
+            self.ms.set_option(getattr(lib, o), getattr(lib, v))
+        try:
+            return self._step(keys, ko)
+        finally:
+            for o, v in saved.items():
+                self.ms.set_option(getattr(lib, o), v)
+
+    def _step(self, keys=None, ko=None):
         keys = self.keys if keys is None else keys
         ko = self.ko if ko is None else ko
         if self.world > 1:  # the library's sharded call (fused KP path: registered windows)
@@ -583,7 +613,9 @@ def sweep(args, dev, flush, hbm):
             [("ms_pairs_c3", 64), ("ms_pairs_c3", 128), ("ms_pairs_c3", 256), ("ms_pairs_c3_skew", 256),
              ("ms_pairs_c3_radix", 64), ("ms_pairs_c3_radix", 128), ("ms_pairs_c3_radix", 256),
              ("ms_pairs_c3_radix_skew", 256),
-             ("sort_keys", 256), ("sort_pairs", 256), ("sort_keys_r5", 32), ("sort_pairs_r5", 32),
+             ("sort_keys", 256), ("sort_pairs", 256), ("sort_keys_passes", 256), ("sort_pairs_passes", 256),
+             ("sort_keys_r5", 32), ("sort_pairs_r5", 32),
+             ("ms_keys_os", 2), ("ms_keys_os", 32), ("ms_keys_os", 256), ("ms_pairs_os", 32), ("ms_pairs_os", 256),
              ("hist_even", 2), ("hist_even", 256), ("hist_range", 2), ("hist_range", 256),
              ("ms_keys_spl", 32), ("ms_keys_spl", 256), ("ms_pairs_spl", 256),
              ("ms_keys_large", 1024), ("ms_keys_large", 65536), ("ms_pairs_large", 4096),
@@ -600,6 +632,8 @@ def sweep(args, dev, flush, hbm):
         e = {"value": round(rate, 2), "unit": wl["unit"], "ms": round(t, 4),
              "hbm_frac": round(rate * us * wl["bpe"] / (hbm * 1e9), 3),
              "hbm_frac_nominal": round(rate * us * wl["bpe"] / (NOMINAL_HBM_GBS * 1e9), 3)}
+        if "bpe_f1" in wl:  # against the one-pass sort's own bound (36 / 68 B)
+            e["hbm_frac_f1"] = round(rate * us * wl["bpe_f1"] / (hbm * 1e9), 3)
         if wl["kind"] == "sssp":
             e["iterations"] = run.sssp_stats()["iterations"]
         if stages:

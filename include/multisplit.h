@@ -101,12 +101,22 @@ int ms_lane_ordered_increment(void);
  *   MS_OPT_PIPELINE:   MS_PIPELINE_LEVEL0 (default: Eq.3 with the CTA ranges
  *                      as level 0, two launches) or MS_PIPELINE_TILE (the
  *                      paper's {tile histograms H, scan of H, postscan},
- *                      P:529-540, three launches).
+ *                      P:529-540, three launches) or MS_PIPELINE_ONESWEEP
+ *                      (bucket counts in one read, then one
+ *                      fused rank / decoupled look-back / scatter kernel;
+ *                      n < 2^30 on a device whose probe held, else LEVEL0).
+ *   MS_OPT_SORT:       MS_SORT_AUTO (default: the radix sort computes every
+ *                      digit histogram in one read and runs one fused
+ *                      look-back pass per digit, 36 B/key for 4 x 8 bits;
+ *                      where n < 2^30, the probe held, <= 8 passes) or
+ *                      MS_SORT_PASSES (every pass a full multisplit,
+ *                      P:1613-1616, 48 B/key).
  * ms_set_option returns MS_ERR_INVALID_VALUE for an unknown option / value;
  * ms_get_option returns the value, or -1 for an unknown option. */
-enum { MS_OPT_RANK = 0, MS_OPT_RUN_STORES = 1, MS_OPT_PIPELINE = 2 };
+enum { MS_OPT_RANK = 0, MS_OPT_RUN_STORES = 1, MS_OPT_PIPELINE = 2, MS_OPT_SORT = 3 };
 enum { MS_RANK_AUTO = 0, MS_RANK_PEER_MASKS = 1 };
-enum { MS_PIPELINE_LEVEL0 = 0, MS_PIPELINE_TILE = 1 };
+enum { MS_PIPELINE_LEVEL0 = 0, MS_PIPELINE_TILE = 1, MS_PIPELINE_ONESWEEP = 2 };
+enum { MS_SORT_AUTO = 0, MS_SORT_PASSES = 1 };
 ms_status ms_set_option(int option, int value);
 int ms_get_option(int option);
 

@@ -122,7 +122,7 @@ def _stream_ptr(stream, device: torch.device | None = None) -> int:
 
 
 def set_option(option: int, value: int) -> None:
-    """ms_set_option (process-wide): MS_OPT_RANK / MS_OPT_RUN_STORES / MS_OPT_PIPELINE."""
+    """ms_set_option (process-wide): MS_OPT_RANK / MS_OPT_RUN_STORES / MS_OPT_PIPELINE / MS_OPT_SORT."""
     check(_lib.load().ms_set_option(option, value), "ms_set_option")
 
 

@@ -22,10 +22,14 @@ MS_ERR_NCCL = 6
 MS_OPT_RANK = 0
 MS_OPT_RUN_STORES = 1
 MS_OPT_PIPELINE = 2
+MS_OPT_SORT = 3
 MS_RANK_AUTO = 0
 MS_RANK_PEER_MASKS = 1
 MS_PIPELINE_LEVEL0 = 0
 MS_PIPELINE_TILE = 1
+MS_PIPELINE_ONESWEEP = 2
+MS_SORT_AUTO = 0
+MS_SORT_PASSES = 1
 
 MS_BUCKET_IDENTITY = 0
 MS_BUCKET_DELTA = 1

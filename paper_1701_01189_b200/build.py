@@ -29,7 +29,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-re
 
 SOURCES = ["ms_capi.cu", "ms_inst_identity.cu", "ms_inst_delta.cu", "ms_inst_radix.cu", "ms_inst_splitters.cu", "ms_sssp.cu",
            "ms_inst_deltashift.cu", "ms_inst_topbits.cu"]
-HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_meta.cuh", "ms_wide.cuh", "ms_large.cuh", "ms_nccl.cuh", "ms_dispatch.cuh", "ms_scan.cuh", "ms_hist.cuh"]
+HEADERS = ["ms_device.cuh", "ms_kernels.cuh", "ms_meta.cuh", "ms_wide.cuh", "ms_onesweep.cuh", "ms_large.cuh", "ms_nccl.cuh", "ms_dispatch.cuh", "ms_scan.cuh", "ms_hist.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

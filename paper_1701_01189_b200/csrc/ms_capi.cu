@@ -29,7 +29,8 @@ namespace ms {
 constexpr int kMaxDevices = 64;
 std::atomic<int> g_probe[kMaxDevices];
 std::mutex g_probe_mu;
-std::atomic<int> g_opt[3] = {{MS_RANK_AUTO}, {1}, {MS_PIPELINE_LEVEL0}};
+constexpr int kNumOpts = 4;
+std::atomic<int> g_opt[kNumOpts] = {{MS_RANK_AUTO}, {1}, {MS_PIPELINE_LEVEL0}, {MS_SORT_AUTO}};
 
 int current_device() {
   int d = 0;
@@ -385,6 +386,75 @@ cudaError_t l0_postscan(const Plan &pl, bool pairs, KfArgs &a, const L0 &st, cud
   return counted(fused_meta_wide(pl, pairs, a, st.G, s));
 }
 
+// ---------------------------------------------------------------- one pass (f1)
+// ms_onesweep.cuh.  Workspace: [hdr 256 B][gh: nbins words][tickets: P words]
+// [status: P x L x 256 words]; everything up to the end of the status words is
+// zeroed by one memset at the start of the call.
+struct OsLayout {
+  size_t gh, tickets, status, total;
+  uint32_t L;
+};
+OsLayout os_layout(uint64_t n, uint32_t passes, bool pairs) {
+  OsLayout lo{};
+  lo.L = (uint32_t)((n + ko_tile(pairs) - 1) / ko_tile(pairs));
+  lo.gh = kHdrBytes;
+  lo.tickets = lo.gh + align_up((size_t)kKoMaxBins * 4u);
+  lo.status = lo.tickets + align_up((size_t)kKoMaxPasses * 4u);
+  lo.total = lo.status + align_up((size_t)passes * lo.L * kKoBins * 4u);
+  return lo;
+}
+
+// the one-pass pipeline ranks with lane-ordered increments (reading R23): only
+// where the device's probe held and deterministic ranks were not requested
+bool onesweep_ok(uint64_t n) {
+  return n > 0 && n < kKoMaxN && g_opt[MS_OPT_RANK].load(std::memory_order_relaxed) == MS_RANK_AUTO &&
+         ms::lane_ordered_inc(false) == 1;
+}
+
+cudaError_t os_pass(const Plan &pl, bool pairs, const uint32_t *ki, const uint32_t *vi, uint32_t *ko,
+                    uint32_t *vo, uint32_t n, const OsLayout &lo, char *w, uint32_t p, uint32_t bin0,
+                    uint32_t *bucket_offsets, cudaStream_t s) {
+  KoArgs a{};
+  a.keys_in = ki;
+  a.vals_in = pairs ? vi : nullptr;
+  a.keys_out = ko;
+  a.vals_out = pairs ? vo : nullptr;
+  a.n = n;
+  a.num_tiles = lo.L;
+  a.gh = (const uint32_t *)(w + lo.gh) + bin0;
+  a.status = (uint32_t *)(w + lo.status) + (size_t)p * lo.L * kKoBins;
+  a.ticket = (uint32_t *)(w + lo.tickets) + p;
+  a.hdr = (uint32_t *)w;
+  a.bucket_offsets = bucket_offsets;
+  a.use_tma = (((uintptr_t)ki & 15u) == 0) && (!pairs || (((uintptr_t)vi & 15u) == 0));
+  const uint32_t grid = std::min((uint32_t)sm_count(), lo.L);
+  return counted(MS_LAUNCH(onesweep, pairs, a, pl.bp, grid, s));
+}
+
+// one-pass multisplit: KOH (the bucket counts) -> KO
+ms_status onesweep_multisplit(const Plan &pl, bool pairs, const uint32_t *ki, const uint32_t *vi,
+                              uint32_t *ko, uint32_t *vo, uint32_t n, uint32_t *bucket_offsets,
+                              char *w, cudaStream_t s) {
+  const OsLayout lo = os_layout(n, 1, pairs);
+  stage_event(0, s);
+  if (cudaMemsetAsync(w, 0, lo.total, s) != cudaSuccess) return MS_ERR_CUDA;
+  KoHistArgs h{};
+  h.keys = ki;
+  h.n = n;
+  h.npass = 1;
+  h.shift[0] = pl.bp.shift;
+  h.mask[0] = pl.bp.mask;
+  h.nbins = pl.bp.m;
+  h.gh = (uint32_t *)(w + lo.gh);
+  h.hdr = (uint32_t *)w;
+  if (counted(MS_LAUNCH(ko_hist, h, pl.bp, (uint32_t)sm_count(), s)) != cudaSuccess) return MS_ERR_CUDA;
+  stage_event(1, s);
+  stage_event(2, s);
+  const cudaError_t e = os_pass(pl, pairs, ki, vi, ko, vo, n, lo, w, 0, 0, bucket_offsets, s);
+  stage_event(3, s);
+  return e == cudaSuccess ? MS_SUCCESS : MS_ERR_CUDA;
+}
+
 // ---------------------------------------------------------------- m > 256
 // Sec.6.3: iterated multisplits over <= 256 buckets, here LSD over
 // the 8-bit digits of the bucket id (ms_large.cuh).  RADIX digits wider than 8
@@ -577,6 +647,9 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   uint32_t *H = (uint32_t *)(w + lo.H);
   a.num_tiles = lo.L;
 
+  if (g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed) == MS_PIPELINE_ONESWEEP && onesweep_ok(n))
+    return onesweep_multisplit(pl, pairs, keys_in, vals_in, keys_out, vals_out, (uint32_t)n,
+                               bucket_offsets, w, s);
   if (g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed) == MS_PIPELINE_TILE) {
     // paper-faithful {local, global, local}: tile histograms H -> scan -> postscan
     unsigned long long *status = (unsigned long long *)(w + lo.status);
@@ -656,6 +729,47 @@ ms_status radix_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
     ms_bytes = x > ms_bytes ? x : ms_bytes;
   }
   char *w = (char *)ws;
+  uint32_t nbins = 0;
+  for (int p = 0; p < passes; ++p) nbins += 1u << bits[p];
+  if (onesweep_ok(n) && passes <= (int)kKoMaxPasses && nbins <= kKoMaxBins &&
+      g_opt[MS_OPT_SORT].load(std::memory_order_relaxed) == MS_SORT_AUTO) {
+    // f1: every digit histogram in one read (KOH), then one KO pass per digit
+    cudaStream_t s = (cudaStream_t)stream;
+    const OsLayout lo = os_layout(n, (uint32_t)passes, pairs);
+    uint32_t *alt_k = (uint32_t *)(w + align_up(lo.total));
+    uint32_t *alt_v = pairs ? (uint32_t *)((char *)alt_k + align_up(n * 4u)) : nullptr;
+    if (cudaMemsetAsync(w, 0, lo.total, s) != cudaSuccess) return MS_ERR_CUDA;
+    KoHistArgs h{};
+    h.keys = keys_in;
+    h.n = (uint32_t)n;
+    h.npass = (uint32_t)passes;
+    uint32_t bin0[kKoMaxPasses];
+    for (int p = 0, b = 0; p < passes; b += 1 << bits[p], ++p) {
+      h.shift[p] = shifts[p];
+      h.mask[p] = (1u << bits[p]) - 1u;
+      h.bin0[p] = bin0[p] = (uint32_t)b;
+    }
+    h.nbins = nbins;
+    h.gh = (uint32_t *)(w + lo.gh);
+    h.hdr = (uint32_t *)w;
+    BucketParams none{};
+    none.m = 256;
+    none.m1 = 255;
+    if (counted(Launch<kRadix>::ko_hist(h, none, (uint32_t)sm_count(), s)) != cudaSuccess) return MS_ERR_CUDA;
+    const uint32_t *src_k = keys_in, *src_v = vals_in;
+    for (int p = 0; p < passes; ++p) {
+      const bool to_out = ((passes - 1 - p) % 2) == 0;
+      uint32_t *dk = to_out ? keys_out : alt_k;
+      uint32_t *dv = to_out ? vals_out : alt_v;
+      const ms_bucket_fn fn{MS_BUCKET_RADIX, 1u << bits[p], 0u, shifts[p], bits[p]};
+      if (os_pass(make_plan(&fn), pairs, src_k, src_v, dk, dv, (uint32_t)n, lo, w, (uint32_t)p, bin0[p],
+                  nullptr, s) != cudaSuccess)
+        return MS_ERR_CUDA;
+      src_k = dk;
+      src_v = dv;
+    }
+    return MS_SUCCESS;
+  }
   uint32_t *alt_k = (uint32_t *)(w + align_up(ms_bytes));
   uint32_t *alt_v = pairs ? (uint32_t *)((char *)alt_k + align_up(n * 4u)) : nullptr;
   // ping-pong so that the last pass lands in the output: ... alt -> out
@@ -713,7 +827,11 @@ ms_status ms_set_option(int option, int value) {
       if (value != 0 && value != 1) return MS_ERR_INVALID_VALUE;
       break;
     case MS_OPT_PIPELINE:
-      if (value != MS_PIPELINE_LEVEL0 && value != MS_PIPELINE_TILE) return MS_ERR_INVALID_VALUE;
+      if (value != MS_PIPELINE_LEVEL0 && value != MS_PIPELINE_TILE && value != MS_PIPELINE_ONESWEEP)
+        return MS_ERR_INVALID_VALUE;
+      break;
+    case MS_OPT_SORT:
+      if (value != MS_SORT_AUTO && value != MS_SORT_PASSES) return MS_ERR_INVALID_VALUE;
       break;
     default: return MS_ERR_INVALID_VALUE;
   }
@@ -722,7 +840,7 @@ ms_status ms_set_option(int option, int value) {
 }
 
 int ms_get_option(int option) {
-  return option >= 0 && option < 3 ? ms::g_opt[option].load(std::memory_order_relaxed) : -1;
+  return option >= 0 && option < ms::kNumOpts ? ms::g_opt[option].load(std::memory_order_relaxed) : -1;
 }
 
 ms_status ms_bucket_delta_default(uint32_t m, ms_bucket_fn *out) {
@@ -756,7 +874,10 @@ size_t ms_multisplit_workspace_size(uint64_t n, uint32_t m, int with_values) {
     const size_t b = large_layout(n, MS_BUCKET_RADIX, with_values != 0).total;
     return a > b ? a : b;
   }
-  return layout_for(n, m, with_values != 0).total;
+  const size_t t = layout_for(n, m, with_values != 0).total;
+  // the one-pass pipeline (MS_PIPELINE_ONESWEEP) on the same workspace
+  const size_t o = n < kKoMaxN ? os_layout(n, 1, with_values != 0).total : 0u;
+  return t > o ? t : o;
 }
 
 ms_status ms_multisplit_keys(const uint32_t *keys_in, uint32_t *keys_out, uint64_t n,
@@ -836,6 +957,11 @@ size_t ms_radix_sort_workspace_size(uint64_t n, int with_values) {
   for (uint32_t r = 1; r <= 8; ++r) {
     const size_t x = ms_multisplit_workspace_size(n, 1u << r, with_values);
     ms_ws = x > ms_ws ? x : ms_ws;
+  }
+  // or the one-pass sort (f1): up to kKoMaxPasses status blocks
+  if (n < kKoMaxN) {
+    const size_t o = os_layout(n, kKoMaxPasses, with_values != 0).total;
+    ms_ws = o > ms_ws ? o : ms_ws;
   }
   return align_up(ms_ws) + align_up(n * 4u) +
          (with_values ? align_up(n * 4u) : 0u);

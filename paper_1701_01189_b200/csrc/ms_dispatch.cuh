@@ -8,6 +8,7 @@
 
 #include "ms_wide.cuh"
 #include "ms_large.cuh"
+#include "ms_onesweep.cuh"
 
 #include <atomic>
 
@@ -70,6 +71,28 @@ struct Launch {
   static cudaError_t merge(bool pairs, const uint32_t *keys, const uint32_t *vals, uint32_t n,
                            const BucketParams &bp, const uint32_t *starts, const uint32_t *offs,
                            uint32_t G, uint32_t *keys_out, uint32_t *vals_out, cudaStream_t s);
+  // one-pass pipeline (ms_onesweep.cuh): bucket histograms of every pass in one
+  // read, then one fused rank / look-back / scatter kernel per pass
+  static cudaError_t ko_hist(const KoHistArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
+    auto kern = ms::ko_hist<KIND>;
+    static std::atomic<unsigned long long> done{0};
+    const size_t smem = (size_t)kKoMaxBins * 32u * 4u;
+    const cudaError_t e = set_max_smem(kern, smem, done);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 1024, (size_t)a.nbins * 32u * 4u, s>>>(a, bp);
+    return cudaGetLastError();
+  }
+  static cudaError_t onesweep(bool pairs, const KoArgs &a, const BucketParams &bp, uint32_t grid,
+                              cudaStream_t s) {
+    auto go = [&](auto kern, bool pr, std::atomic<unsigned long long> &done) {
+      const cudaError_t e = set_max_smem(kern, ko_smem_bytes(pr), done);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, ko_threads(pr), ko_smem_bytes(pr), s>>>(a, bp);
+      return cudaGetLastError();
+    };
+    static std::atomic<unsigned long long> done[2];
+    return pairs ? go(ko_onesweep<KIND, true>, true, done[0]) : go(ko_onesweep<KIND, false>, false, done[1]);
+  }
 };
 
 template <int KIND>

@@ -145,7 +145,8 @@ def test_unaligned_outputs(m):
 def option():
     """Set libms options for one test and restore the defaults afterwards."""
     lib = ms._lib
-    saved = {o: ms.get_option(o) for o in (lib.MS_OPT_RANK, lib.MS_OPT_RUN_STORES, lib.MS_OPT_PIPELINE)}
+    saved = {o: ms.get_option(o) for o in (lib.MS_OPT_RANK, lib.MS_OPT_RUN_STORES, lib.MS_OPT_PIPELINE,
+                                           lib.MS_OPT_SORT)}
     yield ms.set_option
     for o, v in saved.items():
         ms.set_option(o, v)
