@@ -1315,7 +1315,7 @@ NcclLayout nccl_layout(uint64_t n, uint32_t m, uint32_t G, bool pairs) {
   NcclLayout L{};
   L.ms = 0;
   const size_t nb = align_up(n * 4u);
-  L.stage_k = align_up(layout_for(n, m, pairs).total);
+  L.stage_k = align_up(ms_multisplit_workspace_size(n, m, pairs));  // the local multisplit's workspace
   L.stage_v = L.stage_k + nb;
   L.recv_k = L.stage_v + (pairs ? nb : 0);
   L.recv_v = L.recv_k + nb;

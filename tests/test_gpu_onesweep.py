@@ -4,7 +4,7 @@ against the CPU oracle, element by element, bit-exact.
 - the radix sort's default path (MS_SORT_AUTO): every digit histogram in one
   read (KOH), then one fused rank / decoupled look-back / scatter pass (KO)
   per digit -- schedules of 1..8 passes, ragged tails around the KO tile
-  (16384 keys, 8192 pairs), duplicated and skewed keys (the hot-digit ballot
+  (12288 keys, 8192 pairs), duplicated and skewed keys (the hot-digit ballot
   path), unaligned inputs (the non-TMA loads), repeated calls;
 - the one-pass multisplit (MS_PIPELINE_ONESWEEP) over the SPEC m grid and the
   four bucket identifiers, keys and pairs, uniform / skewed / single-bucket,
@@ -21,7 +21,7 @@ from gen import inputs as gen
 pytestmark = pytest.mark.gpu
 
 ms = pytest.importorskip("paper_1701_01189_b200")
-TK, TP = 16384, 8192  # KO tiles: keys (32 warps x 512), pairs (16 x 512)
+TK, TP = 12288, 8192  # KO tiles: keys (24 compute warps x 512), pairs (16 x 512)
 
 
 def dev(a: np.ndarray) -> torch.Tensor:
