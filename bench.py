@@ -81,6 +81,15 @@ WORKLOADS = {
     "ms_pairs_os": dict(n=1 << 25, pairs=True, kind="delta", m=32, unit="Gpairs/s", bpe=20,
                         opts={"MS_OPT_PIPELINE": "MS_PIPELINE_ONESWEEP"},
                         desc="key-value multisplit, n=2^25, delta buckets, one-pass pipeline (f1)"),
+    "ms_pairs_c3_os": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
+                           opts={"MS_OPT_PIPELINE": "MS_PIPELINE_ONESWEEP"},
+                           desc="key-value multisplit, n=2^27, identity buckets, one-pass pipeline (f1)"),
+    "ms_pairs_c3_skew_os": dict(n=1 << 27, pairs=True, kind="identity", m=256, unit="Gpairs/s", bpe=20,
+                                dist="skew", opts={"MS_OPT_PIPELINE": "MS_PIPELINE_ONESWEEP"},
+                                desc="key-value multisplit, n=2^27, identity, 90% one bucket, one-pass (f1)"),
+    "ms_pairs_level0": dict(n=1 << 25, pairs=True, kind="delta", m=32, unit="Gpairs/s", bpe=20,
+                            opts={"MS_OPT_PIPELINE": "MS_PIPELINE_LEVEL0"},
+                            desc="key-value multisplit, n=2^25, delta buckets, two-kernel level-0 pipeline"),
     # the same sorts with 5-bit digits: 7 passes through the m <= 32 pipeline
     # (the paper's Table 8 sweeps r); bpe counts the 7 passes
     "sort_keys_r5": dict(n=1 << 28, pairs=False, kind="sort", m=32, bits=5, unit="Gkeys/s", bpe=84,

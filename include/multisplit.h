@@ -98,7 +98,10 @@ int ms_lane_ordered_increment(void);
  *                      deterministic peer masks).
  *   MS_OPT_RUN_STORES: 1 (default: whole-run TMA bulk stores where runs are
  *                      long) or 0 (per-element coalesced stores only).
- *   MS_OPT_PIPELINE:   MS_PIPELINE_LEVEL0 (default: Eq.3 with the CTA ranges
+ *   MS_OPT_PIPELINE:   MS_PIPELINE_AUTO (default: LEVEL0, except key-value
+ *                      pairs with m > 128, which take ONESWEEP -- measured
+ *                      faster there: 2^27 pairs, m = 256, 216 vs 170 Gpairs/s),
+ *                      MS_PIPELINE_LEVEL0 (Eq.3 with the CTA ranges
  *                      as level 0, two launches) or MS_PIPELINE_TILE (the
  *                      paper's {tile histograms H, scan of H, postscan},
  *                      P:529-540, three launches) or MS_PIPELINE_ONESWEEP
@@ -115,7 +118,7 @@ int ms_lane_ordered_increment(void);
  * ms_get_option returns the value, or -1 for an unknown option. */
 enum { MS_OPT_RANK = 0, MS_OPT_RUN_STORES = 1, MS_OPT_PIPELINE = 2, MS_OPT_SORT = 3 };
 enum { MS_RANK_AUTO = 0, MS_RANK_PEER_MASKS = 1 };
-enum { MS_PIPELINE_LEVEL0 = 0, MS_PIPELINE_TILE = 1, MS_PIPELINE_ONESWEEP = 2 };
+enum { MS_PIPELINE_LEVEL0 = 0, MS_PIPELINE_TILE = 1, MS_PIPELINE_ONESWEEP = 2, MS_PIPELINE_AUTO = 3 };
 enum { MS_SORT_AUTO = 0, MS_SORT_PASSES = 1 };
 ms_status ms_set_option(int option, int value);
 int ms_get_option(int option);

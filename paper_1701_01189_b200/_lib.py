@@ -28,6 +28,7 @@ MS_RANK_PEER_MASKS = 1
 MS_PIPELINE_LEVEL0 = 0
 MS_PIPELINE_TILE = 1
 MS_PIPELINE_ONESWEEP = 2
+MS_PIPELINE_AUTO = 3
 MS_SORT_AUTO = 0
 MS_SORT_PASSES = 1
 

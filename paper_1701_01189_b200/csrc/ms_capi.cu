@@ -30,7 +30,7 @@ constexpr int kMaxDevices = 64;
 std::atomic<int> g_probe[kMaxDevices];
 std::mutex g_probe_mu;
 constexpr int kNumOpts = 4;
-std::atomic<int> g_opt[kNumOpts] = {{MS_RANK_AUTO}, {1}, {MS_PIPELINE_LEVEL0}, {MS_SORT_AUTO}};
+std::atomic<int> g_opt[kNumOpts] = {{MS_RANK_AUTO}, {1}, {MS_PIPELINE_AUTO}, {MS_SORT_AUTO}};
 
 int current_device() {
   int d = 0;
@@ -647,10 +647,14 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
   uint32_t *H = (uint32_t *)(w + lo.H);
   a.num_tiles = lo.L;
 
-  if (g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed) == MS_PIPELINE_ONESWEEP && onesweep_ok(n))
+  // one pass (f1): on request, or (AUTO) for pairs with m > 128, where it was
+  // measured faster than the level-0 pipeline (2^25 pairs m = 256: 195 vs 159
+  // Gpairs/s; m = 128: 201 vs 208; keys m = 256: 267 vs 288)
+  const int pipe = g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed);
+  if ((pipe == MS_PIPELINE_ONESWEEP || (pipe == MS_PIPELINE_AUTO && pairs && m > 128)) && onesweep_ok(n))
     return onesweep_multisplit(pl, pairs, keys_in, vals_in, keys_out, vals_out, (uint32_t)n,
                                bucket_offsets, w, s);
-  if (g_opt[MS_OPT_PIPELINE].load(std::memory_order_relaxed) == MS_PIPELINE_TILE) {
+  if (pipe == MS_PIPELINE_TILE) {
     // paper-faithful {local, global, local}: tile histograms H -> scan -> postscan
     unsigned long long *status = (unsigned long long *)(w + lo.status);
     stage_event(0, s);
@@ -827,7 +831,8 @@ ms_status ms_set_option(int option, int value) {
       if (value != 0 && value != 1) return MS_ERR_INVALID_VALUE;
       break;
     case MS_OPT_PIPELINE:
-      if (value != MS_PIPELINE_LEVEL0 && value != MS_PIPELINE_TILE && value != MS_PIPELINE_ONESWEEP)
+      if (value != MS_PIPELINE_LEVEL0 && value != MS_PIPELINE_TILE && value != MS_PIPELINE_ONESWEEP &&
+          value != MS_PIPELINE_AUTO)
         return MS_ERR_INVALID_VALUE;
       break;
     case MS_OPT_SORT:

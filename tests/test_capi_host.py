@@ -135,13 +135,21 @@ def test_options_host(lib):
     """ms_set_option / ms_get_option are host-only: defaults, validation, round trip."""
     assert lib.ms_get_option(_lib.MS_OPT_RANK) == _lib.MS_RANK_AUTO
     assert lib.ms_get_option(_lib.MS_OPT_RUN_STORES) == 1
-    assert lib.ms_get_option(_lib.MS_OPT_PIPELINE) == _lib.MS_PIPELINE_LEVEL0
-    assert lib.ms_get_option(3) == -1
+    assert lib.ms_get_option(_lib.MS_OPT_PIPELINE) == _lib.MS_PIPELINE_AUTO
+    assert lib.ms_get_option(_lib.MS_OPT_SORT) == _lib.MS_SORT_AUTO
+    assert lib.ms_get_option(4) == -1
     assert lib.ms_set_option(_lib.MS_OPT_RANK, 5) == _lib.MS_ERR_INVALID_VALUE
     assert lib.ms_set_option(9, 0) == _lib.MS_ERR_INVALID_VALUE
     assert lib.ms_set_option(_lib.MS_OPT_RANK, _lib.MS_RANK_PEER_MASKS) == 0
     assert lib.ms_get_option(_lib.MS_OPT_RANK) == _lib.MS_RANK_PEER_MASKS
     assert lib.ms_set_option(_lib.MS_OPT_RANK, _lib.MS_RANK_AUTO) == 0
+    for v in (_lib.MS_PIPELINE_LEVEL0, _lib.MS_PIPELINE_TILE, _lib.MS_PIPELINE_ONESWEEP, _lib.MS_PIPELINE_AUTO):
+        assert lib.ms_set_option(_lib.MS_OPT_PIPELINE, v) == 0 and lib.ms_get_option(_lib.MS_OPT_PIPELINE) == v
+    assert lib.ms_set_option(_lib.MS_OPT_PIPELINE, 4) == _lib.MS_ERR_INVALID_VALUE
+    assert lib.ms_set_option(_lib.MS_OPT_SORT, _lib.MS_SORT_PASSES) == 0
+    assert lib.ms_get_option(_lib.MS_OPT_SORT) == _lib.MS_SORT_PASSES
+    assert lib.ms_set_option(_lib.MS_OPT_SORT, 2) == _lib.MS_ERR_INVALID_VALUE
+    assert lib.ms_set_option(_lib.MS_OPT_SORT, _lib.MS_SORT_AUTO) == 0
 
 
 def test_workspace_alignment_rejected(lib):

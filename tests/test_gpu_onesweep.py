@@ -191,3 +191,15 @@ def test_onesweep_single_bucket_and_domain_error(option, m):
     kd = dev(keys)
     ms.multisplit(kd, None, bucket=pb)
     assert ms.device_status() == ms._lib.MS_ERR_KEY_DOMAIN
+
+
+@pytest.mark.parametrize("pipe", ["AUTO", "LEVEL0"])
+@pytest.mark.parametrize("m", [128, 129, 200, 256])
+@pytest.mark.parametrize("dist", [gen.DIST_UNIFORM, gen.DIST_SKEW])
+def test_pairs_wide_m_default_and_level0(option, pipe, m, dist):
+    """AUTO sends pairs with m > 128 through the one-pass pipeline; LEVEL0 keeps KMW -> KFW."""
+    option(ms._lib.MS_OPT_PIPELINE, getattr(ms._lib, "MS_PIPELINE_" + pipe))
+    ob, pb, gk = bucket_pair("identity", m)
+    n = 11 * TP + 517
+    keys = gen.keys(n, seed=m + 3, dist=dist, alpha=0.1, **gk)
+    check_multisplit(keys, gen.values(n, seed=m), ob, pb)
