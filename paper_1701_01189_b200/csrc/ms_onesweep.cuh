@@ -243,9 +243,6 @@ __device__ unsigned long long ko_lbstat[4];  // windows, spins, -, -
 #ifndef KO_RL
 #define KO_RL 2  // look-back rows per round trip, dedicated look-back warps
 #endif
-#ifndef KO_SCAN2
-#define KO_SCAN2 1
-#endif
 
 // Look-back of tile t for bucket b (Eq.2 term 2): returns sum_{l < t} h_{b,l}
 // and publishes the inclusive prefix of t (tot = h_{b,t}).  v: the status words
@@ -325,9 +322,7 @@ __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1
   __shared__ __align__(8) uint64_t tabr[2];  // LBW: its scatter offsets are ready
   __shared__ uint32_t s_tile[NS];
   __shared__ uint32_t s_lbt[2];  // LBW: tile of the hand-off, ~0u: no more tiles
-  // SCAN2: 512 scan threads, two per bucket (keys: the producer stays outside)
-  constexpr bool SCAN2 = KO_SCAN2 && LBW > 0 && NC - 32u >= 2u * NB && W % 2u == 0u;
-  __shared__ uint32_t s_wsum[2u * NB / 32u];
+  __shared__ uint32_t s_wsum[NB / 32u];
   __shared__ uint32_t s_hot;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   constexpr uint32_t kProducer = NC - 32u;  // outside the scan threads
@@ -541,48 +536,12 @@ __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1
       fence_proxy_async_smem();
       issue((k + 1u) % NS, atomicAdd(a.ticket, 1u));
     }
-    // ---- per bucket: tile count (publish), first look-back window, scan.
-    // SCAN2 (keys): two threads per bucket (lanes 2i, 2i+1 of warp w own bucket
-    // 16 w + i), each totalling and rewriting half of the W rows
+    // ---- per bucket: tile count (publish), first look-back window, scan
+    // (two threads per bucket, each half of the rows, measured slower: the
+    // pair shares the bucket's bank)
     uint32_t tot = 0, tb = 0;
     uint32_t v[R];  // status words of tiles t-1 .. t-R (thread b's bucket)
-    if constexpr (SCAN2) {
-      if (tid < 2u * NB) {
-        const uint32_t b = (warp << 4) | (lane >> 1), h = lane & 1u;
-        constexpr uint32_t HW = W / 2u;
-        uint32_t *col = cnt + (h * HW) * NB + b;
-        uint32_t half = 0;
-#pragma unroll
-        for (uint32_t w = 0; w < HW; ++w) half += col[w * NB];
-        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, half, 1);
-        tot = half + other;
-        if (h == 0) st_relaxed_u32(a.status + (size_t)t * NB + b, (t == 0 ? kKoFlagInc : kKoFlagAgg) | tot);
-        uint32_t incl = tot;  // inclusive scan over the warp's 16 buckets (pairs of lanes)
-#pragma unroll
-        for (int o = 2; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= (uint32_t)o) incl += y;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        tb = incl - tot;
-        named_barrier_sync(kBarS, 2u * NB);  // B2
-#pragma unroll
-        for (uint32_t j = 0; j < 2u * NB / 32u; ++j) tb += j < warp ? s_wsum[j] : 0u;
-        uint32_t run = tb + (h ? other : 0u);
-#pragma unroll
-        for (uint32_t w = 0; w < HW; ++w) {
-          const uint32_t c = col[w * NB];
-          col[w * NB] = run;
-          run += c;
-        }
-        if (h == 0) {  // hand the tile to the look-back warps
-          s_tot[(k & 1u) * NB + b] = tot;
-          s_tb[(k & 1u) * NB + b] = tb;
-          if (tid == 0) s_lbt[k & 1u] = t;
-          mbar_arrive(&aggb[k & 1u]);
-        }
-      }
-    } else if (tid < NB) {
+    if (tid < NB) {
 #pragma unroll 8
       for (uint32_t w = 0; w < W; ++w) tot += cnt[w * NB + tid];
       st_relaxed_u32(a.status + (size_t)t * NB + tid, (t == 0 ? kKoFlagInc : kKoFlagAgg) | tot);

@@ -4,7 +4,7 @@
 // per-phase cycles of KO's compute warps.  Development tool, not the product:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -I paper_1701_01189_b200/csrc scripts/ko_harness.cu -o /tmp/koh
-//   /tmp/koh [log2 n] [pairs] [reps]
+//   /tmp/koh [log2 n] [pairs] [reps] [max grid] [n]
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -27,7 +27,7 @@ __global__ void fill(uint32_t *k, uint32_t *v, uint32_t n, uint32_t seed) {
 }
 
 template <bool PAIRS>
-int run(uint32_t n, int reps) {
+int run(uint32_t n, int reps, uint32_t max_grid) {
   uint32_t *k, *v = nullptr, *ko, *vo = nullptr, *ws;
   const uint32_t T = ko_tile(PAIRS), L = (n + T - 1) / T;
   const uint32_t Lpad = (L + 7u) & ~7u;
@@ -76,7 +76,8 @@ int run(uint32_t n, int reps) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
-  const uint32_t grid = L < (uint32_t)sms ? L : (uint32_t)sms;
+  uint32_t grid = L < (uint32_t)sms ? L : (uint32_t)sms;
+  if (max_grid && grid > max_grid) grid = max_grid;  // several tiles per CTA at small n (sanitizers)
   float th = 0, tk = 0;
 #ifdef MS_KO_TIMING
   {
@@ -150,5 +151,7 @@ int main(int argc, char **argv) {
   const int lg = argc > 1 ? atoi(argv[1]) : 25;
   const int pairs = argc > 2 ? atoi(argv[2]) : 0;
   const int reps = argc > 3 ? atoi(argv[3]) : 10;
-  return pairs ? run<true>(1u << lg, reps) : run<false>(1u << lg, reps);
+  const uint32_t max_grid = argc > 4 ? (uint32_t)atoi(argv[4]) : 0u;
+  const uint32_t n = argc > 5 ? (uint32_t)atoi(argv[5]) : (1u << lg);  // explicit n (ragged tails)
+  return pairs ? run<true>(n, reps, max_grid) : run<false>(n, reps, max_grid);
 }
