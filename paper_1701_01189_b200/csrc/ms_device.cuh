@@ -196,6 +196,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// the same, with a suspend-time hint: a waiting thread may sleep (up to the hint,
+// in ns) until the phase completes instead of re-polling (long waits of idle warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)
+        : "memory");
+  } while (!ok);
+}
+
 // 1-D bulk copy global -> shared through the TMA engine (SASS UBLKCP); bytes
 // and both addresses must be multiples of 16.  Completion is signalled on
 // `bar` as transaction bytes.  L2 policy: evict_first for streamed input.

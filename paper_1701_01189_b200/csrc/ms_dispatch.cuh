@@ -74,13 +74,18 @@ struct Launch {
   // one-pass pipeline (ms_onesweep.cuh): bucket histograms of every pass in one
   // read, then one fused rank / look-back / scatter kernel per pass
   static cudaError_t ko_hist(const KoHistArgs &a, const BucketParams &bp, uint32_t grid, cudaStream_t s) {
-    auto kern = ms::ko_hist<KIND>;
-    static std::atomic<unsigned long long> done{0};
-    const size_t smem = (size_t)kKoMaxBins * 32u * 4u;
-    const cudaError_t e = set_max_smem(kern, smem, done);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, 1024, (size_t)a.nbins * 32u * 4u, s>>>(a, bp);
-    return cudaGetLastError();
+    // the 4 x 8-bit sort (digits = the key's bytes) has its own unrolled kernel
+    bool bytes = KIND == kRadix && a.npass == 4u;
+    for (uint32_t p = 0; p < a.npass && bytes; ++p)
+      bytes = a.shift[p] == 8u * p && a.mask[p] == 255u && a.bin0[p] == 256u * p;
+    auto go = [&](auto kern, std::atomic<unsigned long long> &done) {
+      const cudaError_t e = set_max_smem(kern, (size_t)kKoMaxBins * 32u * 4u, done);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, 1024, (size_t)a.nbins * 32u * 4u, s>>>(a, bp);
+      return cudaGetLastError();
+    };
+    static std::atomic<unsigned long long> done[2];
+    return bytes ? go(ms::ko_hist<KIND, true>, done[0]) : go(ms::ko_hist<KIND, false>, done[1]);
   }
   static cudaError_t onesweep(bool pairs, const KoArgs &a, const BucketParams &bp, uint32_t grid,
                               cudaStream_t s) {

@@ -95,7 +95,7 @@ __device__ __forceinline__ void red_shared_inc(uint32_t saddr) {
 // once per 16 keys.  Non-RADIX kinds (the one-pass multisplit) have one pass,
 // f = bucket_of<KIND>.
 // ============================================================================
-template <int KIND>
+template <int KIND, bool BYTES>
 __global__ void __launch_bounds__(1024, 1) ko_hist(KoHistArgs a, BucketParams bp) {
   MS_STAGE_SPLITTERS(bp, kMaxBuckets);
   extern __shared__ __align__(16) uint32_t koh_cnt[];  // [nbins][32]
@@ -105,7 +105,15 @@ __global__ void __launch_bounds__(1024, 1) ko_hist(KoHistArgs a, BucketParams bp
   const uint32_t cbase = smem_u32(koh_cnt) + lane * 4u;
   bool derr = false;
   auto count = [&](const uint32_t *u, int cnt) {
-    if constexpr (KIND == kRadix) {
+    if constexpr (KIND == kRadix && BYTES) {
+      // the 4 x 8-bit sort: digit p is byte p (one PRMT), bins of pass p at
+      // the constant offset p * 256 * 32 words (an immediate of the reduction)
+#pragma unroll
+      for (uint32_t p = 0; p < 4; ++p)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < cnt) red_shared_inc(cbase + (__byte_perm(u[j], 0u, 0x4440u + p) << 7) + p * 256u * 128u);
+    } else if constexpr (KIND == kRadix) {
 #pragma unroll 1
       for (uint32_t p = 0; p < a.npass; ++p) {
         const uint32_t sh = a.shift[p], mk = a.mask[p], b0 = cbase + (a.bin0[p] << 7);
@@ -242,6 +250,14 @@ __device__ unsigned long long ko_lbstat[4];  // windows, spins, -, -
 #endif
 #ifndef KO_RL
 #define KO_RL 2  // look-back rows per round trip, dedicated look-back warps
+#endif
+#ifndef KO_SLEEP
+#define KO_SLEEP 1
+#endif
+#if KO_SLEEP
+#define KO_WAIT(b, p) mbar_wait_sleep(b, p)
+#else
+#define KO_WAIT(b, p) mbar_wait(b, p)
 #endif
 
 // Look-back of tile t for bucket b (Eq.2 term 2): returns sum_{l < t} h_{b,l}
@@ -393,7 +409,7 @@ __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1
       const uint32_t gb = s_gb[lb];
       for (uint32_t i = 0;; ++i) {
         const uint32_t par = i & 1u;
-        mbar_wait(&aggb[par], (i >> 1) & 1u);
+        KO_WAIT(&aggb[par], (i >> 1) & 1u);
         const uint32_t t = s_lbt[par];
         if (t == ~0u) break;
         constexpr uint32_t RL = KO_RL;
@@ -419,7 +435,7 @@ __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1
   };
   // ---- coalesced scatter of a placed tile: slot s of bucket b -> tab[b] + s
   auto scatter = [&](uint32_t t, uint32_t it) {  // tile t of iteration it
-    if constexpr (LBW > 0) mbar_wait(&tabr[it & 1u], (it >> 1) & 1u);
+    if constexpr (LBW > 0) KO_WAIT(&tabr[it & 1u], (it >> 1) & 1u);
     const uint32_t *s_stage = stage0 + (it % NS) * SWD;
     const uint32_t *tab = s_tab + (it & 1u) * NB;
     const uint32_t tn = tile_n(t);

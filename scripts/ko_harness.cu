@@ -68,14 +68,55 @@ int run(uint32_t n, int reps, uint32_t max_grid) {
   a.status = ws + 256 + 1024 + 64;
   a.hdr = ws;
   a.use_tma = 1;
-  auto kh = ko_hist<kRadix>;
+  auto kh = ko_hist<kRadix, false>;
+  auto kh4 = ko_hist<kRadix, true>;
   auto kk = ko_onesweep<kRadix, PAIRS>;
   CK(cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 32 * 4));
+  CK(cudaFuncSetAttribute(kh4, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 32 * 4));
   CK(cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ko_smem_bytes(PAIRS)));
   cudaEvent_t e0, e1, e2;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
+  {  // the 4 x 8-bit sort's histogram: generic vs byte kernel
+    KoHistArgs h4 = h;
+    uint32_t *gh4;
+    CK(cudaMalloc(&gh4, 1024 * 4));
+    h4.npass = 4;
+    h4.nbins = 1024;
+    h4.gh = gh4;
+    for (int p = 0; p < 4; ++p) {
+      h4.shift[p] = 8 * p;
+      h4.mask[p] = 255;
+      h4.bin0[p] = 256 * p;
+    }
+    std::vector<uint32_t> r0(1024), r1(1024);
+    float tg = 0, tb = 0;
+    for (int r = 0; r < 4; ++r) {
+      CK(cudaMemset(gh4, 0, 4096));
+      CK(cudaEventRecord(e0));
+      kh<<<sms, 1024, 1024 * 32 * 4>>>(h4, bp);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaMemcpy(r0.data(), gh4, 4096, cudaMemcpyDeviceToHost));
+      CK(cudaMemset(gh4, 0, 4096));
+      CK(cudaEventRecord(e1));
+      kh4<<<sms, 1024, 1024 * 32 * 4>>>(h4, bp);
+      CK(cudaEventRecord(e2));
+      CK(cudaEventSynchronize(e2));
+      CK(cudaMemcpy(r1.data(), gh4, 4096, cudaMemcpyDeviceToHost));
+      float x, y;
+      CK(cudaEventElapsedTime(&x, e0, e1));
+      CK(cudaEventElapsedTime(&y, e1, e2));
+      if (r) {
+        tg += x;
+        tb += y;
+      }
+    }
+    printf("KOH 4 x 8-bit: generic %.1f us, byte kernel %.1f us, %s\n", tg / 3 * 1e3, tb / 3 * 1e3,
+           r0 == r1 ? "equal counts" : "COUNTS DIFFER");
+    CK(cudaFree(gh4));
+  }
   uint32_t grid = L < (uint32_t)sms ? L : (uint32_t)sms;
   if (max_grid && grid > max_grid) grid = max_grid;  // several tiles per CTA at small n (sanitizers)
   float th = 0, tk = 0;

@@ -203,3 +203,13 @@ def test_pairs_wide_m_default_and_level0(option, pipe, m, dist):
     n = 11 * TP + 517
     keys = gen.keys(n, seed=m + 3, dist=dist, alpha=0.1, **gk)
     check_multisplit(keys, gen.values(n, seed=m), ob, pb)
+
+
+@pytest.mark.parametrize("pairs", [False, True])
+def test_sort_many_tiles_per_cta(pairs):
+    """Past 148 tiles per launch: every persistent CTA takes several tiles (ticket order,
+    deferred scatter, stage reuse, look-back across CTAs), element by element."""
+    n = 148 * 3 * TK + 4099
+    keys = gen.keys(n, seed=41)
+    keys[::7] &= np.uint32(0xFFFF00FF)
+    check_sort(keys, gen.values(n, seed=41) if pairs else None)
