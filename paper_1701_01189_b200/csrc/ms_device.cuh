@@ -43,7 +43,19 @@ struct BucketParams {
   uint32_t spl_pow;          // SPLITTERS: smallest power of two >= m
   const uint32_t *spl;       // SPLITTERS: the m-1 interior splitters s_1 < ... < s_{m-1}
                              // (global on entry; kernels re-point it at a shared copy)
+  const uint32_t *cell;      // SPLITTERS, staged: cell table over the key's top bits, or null
+  uint32_t cell_shift;       // 32 - log2(cells)
+  uint32_t spl_s, cell_s;    // the staged tables' shared-window addresses (ld.shared: a generic
+                             // pointer into shared memory costs a generic load per probe)
 };
+
+// volatile: a plain asm statement may be speculated out of its guard (a kernel
+// whose table is not staged then loads from a garbage shared address)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
 
 // SPLITTERS (reading R27): f(u) = the j with s_j <= u <
 // s_{j+1}, s_0 = 0 and s_m = 2^32 the ends of the key domain, i.e. the number
@@ -54,6 +66,28 @@ struct BucketParams {
 // serialized them: measured 136 Gkeys/s at m = 32)
 template <int DEPTH = 8>
 __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketParams &p) {
+  if (p.cell_shift) {  // staged (a shared-window address may be 0)
+    // the cell of u's top bits holds the splitter indices [A, B): those of the
+    // splitters inside the cell (A = the number below it).  For splitters spread
+    // over the key domain a cell holds none or one (m = 256: 0.25 on average
+    // with 1024 cells), so the bucket costs one table load and at most a
+    // compare; crowded cells fall back to the search below.
+    const uint32_t x = lds_u32(p.cell_s + ((u >> p.cell_shift) << 2));
+    uint32_t j = x & 0xFFFFu;
+    const uint32_t e = x >> 16;
+    if (e - j <= 2u) {
+      if (j < e && lds_u32(p.spl_s + (j << 2)) <= u) ++j;
+      if (j < e && lds_u32(p.spl_s + (j << 2)) <= u) ++j;
+      return j;
+    }
+    uint32_t k = 0;  // crowded cell: the branch-free search over the staged table
+#pragma unroll
+    for (int q = DEPTH - 1; q >= 0; --q) {
+      const uint32_t t = k + (1u << q);
+      if (t <= p.m1 && lds_u32(p.spl_s + ((t - 1u) << 2)) <= u) k = t;
+    }
+    return k;
+  }
   uint32_t j = 0;
 #pragma unroll
   for (int k = DEPTH - 1; k >= 0; --k) {
@@ -66,12 +100,35 @@ __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketPara
 // Every kernel templated on the bucket kind starts with this: for SPLITTERS it
 // copies the table into shared memory (CAP >= m-1 entries) and re-points
 // bp.spl at the copy, so that the per-key search probes shared memory.
+// It also builds the cell table: CAP >= 256 (m <= 256) 1024 cells of the top 10
+// bits (4 KB), smaller tables 128 cells (512 B); cell c = [A_c | A_{c+1} << 16]
+// with A_c = the number of splitters below c << cell_shift (A_cells = m - 1).
 #define MS_STAGE_SPLITTERS(bp_, CAP)                                            \
   if constexpr (KIND == kSplitters) {                                           \
+    constexpr uint32_t ms_cb_ = (CAP) >= 256 ? 10u : 7u;                        \
     __shared__ uint32_t ms_s_spl[CAP];                                          \
+    __shared__ uint32_t ms_s_cell[1u << ms_cb_];                                \
     for (uint32_t i_ = threadIdx.x; i_ < (bp_).m1 && i_ < (CAP); i_ += blockDim.x) \
       ms_s_spl[i_] = __ldg((bp_).spl + i_);                                     \
     __syncthreads();                                                            \
+    if ((bp_).m1 <= (CAP)) {                                                    \
+      for (uint32_t c_ = threadIdx.x; c_ < (1u << ms_cb_); c_ += blockDim.x) {  \
+        const uint64_t lo_ = (uint64_t)c_ << (32u - ms_cb_);                    \
+        const uint64_t hi_ = (uint64_t)(c_ + 1u) << (32u - ms_cb_);             \
+        uint32_t a_ = 0, b_ = 0; /* splitters below lo_ / hi_ (lower bounds) */ \
+        for (int k_ = 7; k_ >= 0; --k_) {                                       \
+          const uint32_t ta_ = a_ + (1u << k_), tb_ = b_ + (1u << k_);          \
+          if (ta_ <= (bp_).m1 && ms_s_spl[ta_ - 1u] < lo_) a_ = ta_;            \
+          if (tb_ <= (bp_).m1 && ms_s_spl[tb_ - 1u] < hi_) b_ = tb_;            \
+        }                                                                       \
+        ms_s_cell[c_] = a_ | (b_ << 16);                                        \
+      }                                                                         \
+      __syncthreads();                                                          \
+      (bp_).cell = ms_s_cell;                                                   \
+      (bp_).cell_shift = 32u - ms_cb_;                                          \
+      (bp_).cell_s = smem_u32(ms_s_cell);                                       \
+      (bp_).spl_s = smem_u32(ms_s_spl);                                         \
+    }                                                                           \
     (bp_).spl = ms_s_spl;                                                       \
   }
 

@@ -318,8 +318,7 @@ __device__ __forceinline__ uint32_t ko_lookback(uint32_t *status, uint32_t t, ui
 template <int KIND, bool PAIRS>
 __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1)
     ko_onesweep(KoArgs a, BucketParams bp) {
-  // (splitter tables are searched in global memory, L1-resident: the keys'
-  // stages leave no room for a staged copy)
+  MS_STAGE_SPLITTERS(bp, kMaxBuckets);  // 1 KB of splitters + the 4 KB cell table
   constexpr uint32_t W = ko_warps(PAIRS), NC = W * 32u, ITEMS = 16u, T = NC * ITEMS;
   constexpr uint32_t LBW = ko_lb_warps(PAIRS);
   constexpr uint32_t SWD = T * (PAIRS ? 2u : 1u);  // words per stage

@@ -133,3 +133,38 @@ def test_large_m_identity_domain_error():
 def test_large_m_limits():
     with pytest.raises(ms.MultisplitError):
         ms.multisplit(dev(np.arange(10, dtype=np.uint32)), bucket=ms.Identity(65537))
+
+
+@pytest.mark.parametrize("layout", ["clustered", "half", "cell_edges", "top_cell", "pairs_per_cell"])
+@pytest.mark.parametrize("m", [32, 256])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_splitter_cell_table(layout, m, pairs):
+    """The staged cell table over the key's top bits (1024 cells for m <= 256
+    kernels, 128 for the m <= 32 ones): crowded cells take the search, cell
+    boundaries and the last cell are exact, cells with two splitters compare twice."""
+    r = np.random.default_rng(m + len(layout))
+    if layout == "clustered":    # every splitter in one cell: the fallback search
+        spl = np.sort(r.choice(1 << 20, size=m - 1, replace=False).astype(np.uint32) + np.uint32(5 << 22))
+    elif layout == "half":       # half crowded, half spread
+        a = r.choice(1 << 18, size=(m - 1) // 2, replace=False).astype(np.uint64) + (7 << 22)
+        b = r.choice(1 << 32, size=m - 1 - a.size, replace=False).astype(np.uint64)
+        spl = np.unique(np.concatenate([a, b])).astype(np.uint32)
+    elif layout == "cell_edges":  # splitters exactly on cell starts (2^22 and 2^25 multiples) and one below
+        c = np.sort(r.choice(1024, size=(m - 1) // 2, replace=False)).astype(np.uint64)
+        spl = np.unique(np.concatenate([c << 22, (c << 22) + 1, [(1 << 32) - 1]])).astype(np.uint32)
+    elif layout == "top_cell":   # splitters near the top of the key domain
+        spl = np.sort((np.uint64(1 << 32) - 1 - r.choice(1 << 21, size=m - 1, replace=False).astype(np.uint64))
+                      .astype(np.uint32))
+    else:                        # exactly two splitters per cell in some cells
+        c = np.sort(r.choice(1024, size=(m - 1) // 2, replace=False)).astype(np.uint64)
+        spl = np.unique(np.concatenate([(c << 22) + 100, (c << 22) + 200])).astype(np.uint32)
+    spl = spl[: m - 1]
+    mm = spl.size + 1
+    n = 5 * 8192 + 333
+    keys = gen.keys(n, seed=mm)
+    k = n // 3  # a third of the keys on, just below and just above the splitters
+    pick = r.integers(0, spl.size, k)
+    edge = spl[pick].astype(np.int64) + r.integers(-1, 2, k)
+    keys[r.choice(n, k, replace=False)] = np.clip(edge, 0, 0xFFFFFFFF).astype(np.uint32)
+    vals = gen.values(n, seed=2) if pairs else None
+    check(keys, vals, oracle.splitters(spl), ms.Splitters(dev(spl)))
