@@ -916,12 +916,12 @@ static ms_status histogram_impl(const float *x, uint64_t n, uint32_t m, float lo
   uint32_t per = (uint32_t)((n + target - 1) / target);
   per = (per + 4095u) & ~4095u;  // whole 16-byte vectors per CTA, >= 4096 samples
   const uint32_t grid = (uint32_t)((n + per - 1) / per);
-  const size_t smem = ((size_t)kWarps * m + m + 1) * 4u;
+  const size_t smem = ((size_t)kWarps * m + m + 1 + (range ? kHistCells : 0u)) * 4u;
   int ex = 0;
   const bool pow2 = std::frexp((float)delta, &ex) == 0.5f && std::isnormal((float)delta) &&
                     std::isnormal(1.0f / (float)delta);
-  if (range)
-    kh_histogram<true, false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, 0.f, 0.f, 0.f,
+  if (range)  // the kernel derives the cell scale cells / (s_m - s_0) itself (delta < 0: unset)
+    kh_histogram<true, false><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, 0.f, 0.f, -1.f,
                                                            splitters, counts);
   else if (pow2)  // exact: multiply by the power-of-two reciprocal
     kh_histogram<false, true><<<grid, kThreads, smem, s>>>(x, (uint32_t)n, per, m, lower, upper,

@@ -72,3 +72,33 @@ def test_full_size_and_errors():
         ms.histogram_even(xd, 257, 0.0, 1024.0)
     with pytest.raises(Exception):
         ms.histogram_even(xd, 8, 1.0, 1.0)
+
+
+@pytest.mark.parametrize("layout", ["crowded", "half_crowded", "huge_span", "tiny_span", "geometric", "cell_edges"])
+@pytest.mark.parametrize("m", [8, 256])
+def test_range_cell_table(layout, m):
+    """Range cells (1024 cells of [s_0, s_m)): crowded cells take the search, a span
+    that overflows binary32 disables the table, cell boundaries are exact."""
+    r = np.random.default_rng(m + len(layout))
+    if layout == "crowded":         # every interior splitter within one cell
+        s = np.concatenate([[0.0], np.sort(r.uniform(500.0, 500.5, m - 1)), [1024.0]])
+    elif layout == "half_crowded":
+        a = np.sort(r.uniform(3.0, 3.01, (m - 1) // 2))
+        b = np.sort(r.uniform(10.0, 1000.0, m - 1 - a.size))
+        s = np.concatenate([[0.0], a, b, [1024.0]])
+    elif layout == "huge_span":     # s_m - s_0 overflows binary32
+        s = np.concatenate([[-3.0e38], np.sort(r.uniform(-1e38, 1e38, m - 1)), [3.0e38]])
+    elif layout == "tiny_span":     # a few ulps wide
+        s = np.float32(1.0) + np.arange(m + 1, dtype=np.float32) * np.float32(2.0 ** -23)
+    elif layout == "geometric":     # log-spaced: many splitters in the low cells
+        s = np.concatenate([[0.0], np.geomspace(1e-6, 1000.0, m - 1), [1024.0]])
+    else:                           # interior splitters exactly on cell starts (s_0 = 0, s_m = 1024)
+        s = np.concatenate([[0.0], np.sort(r.choice(np.arange(1, 1024), m - 1, replace=False)).astype(np.float64),
+                            [1024.0]])
+    s = np.unique(np.asarray(s, np.float32))
+    if s.size < 2:
+        pytest.skip("degenerate splitters")
+    x = np.concatenate([gen.floats(200003, seed=m) * np.float32((s[-1] - s[0]) / 1024.0 if np.isfinite(s[-1] - s[0]) else 1.0)
+                        + s[0], edges(s), r.uniform(float(s[0]), float(s[-1]), 5000).astype(np.float32)]).astype(np.float32)
+    got = host(ms.histogram_range(torch.from_numpy(x).cuda(), torch.from_numpy(s).cuda()))
+    assert np.array_equal(got, oracle.histogram_range(x, s))
