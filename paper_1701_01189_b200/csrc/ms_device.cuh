@@ -64,6 +64,19 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
 // DEPTH = log2 of the largest table (8: m <= 256); the probes are unrolled so
 // that the searches of a thread's keys interleave (a runtime-bounded loop
 // serialized them: measured 136 Gkeys/s at m = 32)
+// crowded cell (more than two splitters): the branch-free search over the
+// staged table, out of line so that the common path is not if-converted into it
+template <int DEPTH>
+__device__ __noinline__ uint32_t splitter_search_staged(uint32_t u, uint32_t spl_s, uint32_t m1) {
+  uint32_t k = 0;
+#pragma unroll
+  for (int q = DEPTH - 1; q >= 0; --q) {
+    const uint32_t t = k + (1u << q);
+    if (t <= m1 && lds_u32(spl_s + ((t - 1u) << 2)) <= u) k = t;
+  }
+  return k;
+}
+
 template <int DEPTH = 8>
 __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketParams &p) {
   if (p.cell_shift) {  // staged (a shared-window address may be 0)
@@ -71,22 +84,16 @@ __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketPara
     // splitters inside the cell (A = the number below it).  For splitters spread
     // over the key domain a cell holds none or one (m = 256: 0.25 on average
     // with 1024 cells), so the bucket costs one table load and at most a
-    // compare; crowded cells fall back to the search below.
+    // compare or two.
     const uint32_t x = lds_u32(p.cell_s + ((u >> p.cell_shift) << 2));
-    uint32_t j = x & 0xFFFFu;
-    const uint32_t e = x >> 16;
-    if (e - j <= 2u) {
-      if (j < e && lds_u32(p.spl_s + (j << 2)) <= u) ++j;
-      if (j < e && lds_u32(p.spl_s + (j << 2)) <= u) ++j;
-      return j;
+    const uint32_t j = x & 0xFFFFu, e = x >> 16;
+    if (e - j > 2u) return splitter_search_staged<DEPTH>(u, p.spl_s, p.m1);
+    uint32_t r = j;
+    if (j < e && lds_u32(p.spl_s + (j << 2)) <= u) {
+      r = j + 1u;
+      if (j + 1u < e && lds_u32(p.spl_s + ((j + 1u) << 2)) <= u) r = j + 2u;
     }
-    uint32_t k = 0;  // crowded cell: the branch-free search over the staged table
-#pragma unroll
-    for (int q = DEPTH - 1; q >= 0; --q) {
-      const uint32_t t = k + (1u << q);
-      if (t <= p.m1 && lds_u32(p.spl_s + ((t - 1u) << 2)) <= u) k = t;
-    }
-    return k;
+    return r;
   }
   uint32_t j = 0;
 #pragma unroll

@@ -33,6 +33,16 @@ __device__ __forceinline__ uint32_t hist_cell(float v, float s0, float inv) {
   return q < (float)(kHistCells - 1) ? (uint32_t)q : kHistCells - 1;  // q >= 0
 }
 
+// crowded cell: the branch-free binary search (out of line: the common path
+// stays free of its predicated steps)
+__device__ __noinline__ uint32_t hist_range_search(float v, uint32_t m, const float *spl) {
+  uint32_t j = 0;  // largest j with spl[j] <= v (spl[0] <= v < spl[m])
+#pragma unroll
+  for (uint32_t step = 128; step >= 1; step >>= 1)
+    if (j + step < m && spl[j + step] <= v) j += step;
+  return j;
+}
+
 template <bool RANGE, bool POW2 = false>
 __device__ __forceinline__ void hist_sample(float v, uint32_t m, float lower, float upper,
                                             float delta, const float *spl, uint32_t *row,
@@ -42,18 +52,16 @@ __device__ __forceinline__ void hist_sample(float v, uint32_t m, float lower, fl
     if (!(v >= lower && v < upper)) return;  // Range: lower = s_0, upper = s_m (registers)
     // cell c = [A | B << 16]: the interior splitters s_{A+1} .. s_B lie in c
     const uint32_t x = cell ? cell[hist_cell(v, lower, delta)] : 0xFFFF0000u;
-    uint32_t j = x & 0xFFFFu;
-    const uint32_t e = x >> 16;
-    if (e - j <= 2u) {
-      if (j < e && spl[j + 1] <= v) ++j;
-      if (j < e && spl[j + 1] <= v) ++j;
+    const uint32_t j = x & 0xFFFFu, e = x >> 16;
+    if (e - j > 2u) {
+      b = hist_range_search(v, m, spl);
     } else {
-      j = 0;  // largest j with spl[j] <= v (spl[0] <= v < spl[m])
-#pragma unroll
-      for (uint32_t step = 128; step >= 1; step >>= 1)
-        if (j + step < m && spl[j + step] <= v) j += step;
+      b = j;
+      if (j < e && spl[j + 1] <= v) {
+        b = j + 1u;
+        if (j + 1u < e && spl[j + 2] <= v) b = j + 2u;
+      }
     }
-    b = j;
   } else {
     if (!(v >= lower && v < upper)) return;
     const float q = POW2 ? __fmul_rn(__fsub_rn(v, lower), delta) : __fdiv_rn(__fsub_rn(v, lower), delta);
