@@ -213,3 +213,54 @@ def test_sort_many_tiles_per_cta(pairs):
     keys = gen.keys(n, seed=41)
     keys[::7] &= np.uint32(0xFFFF00FF)
     check_sort(keys, gen.values(n, seed=41) if pairs else None)
+
+
+@pytest.mark.parametrize("what", ["sort_keys", "sort_pairs", "ms_pairs_256"])
+def test_one_pass_in_cuda_graph(what):
+    """The one-pass pipeline captured in a CUDA graph and replayed on new inputs: the
+    memset node re-zeroes the tickets and look-back words on every replay."""
+    n = 20 * TK + 11
+    pairs = what != "sort_keys"
+    ks = torch.empty(n, dtype=torch.int32, device="cuda")
+    vs = torch.empty(n, dtype=torch.int32, device="cuda") if pairs else None
+    ko = torch.empty_like(ks)
+    vo = torch.empty_like(vs) if pairs else None
+    gk = {}
+    if what == "ms_pairs_256":
+        ob, pb, gk = bucket_pair("identity", 256)
+        off = torch.empty(257, dtype=torch.int32, device="cuda")
+        ws = torch.empty(ms.workspace_size(n, 256, True), dtype=torch.uint8, device="cuda")
+        call = lambda: ms.multisplit(ks, vs, bucket=pb, out_keys=ko, out_values=vo,  # noqa: E731
+                                     out_offsets=off, workspace=ws)
+    else:
+        ws = torch.empty(ms.radix_sort_workspace_size(n, pairs), dtype=torch.uint8, device="cuda")
+        call = lambda: ms.radix_sort(ks, vs, bits_per_pass=8, out_keys=ko, out_values=vo,  # noqa: E731
+                                     workspace=ws)
+    ms.device_init(0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside the capture (kernel attributes)
+        ks.copy_(dev(gen.keys(n, seed=1, **gk)))
+        if pairs:
+            vs.copy_(dev(gen.values(n, seed=1)))
+        call()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        call()
+    for seed in (2, 3, 4):
+        kh = gen.keys(n, seed=seed, **gk)
+        vh = gen.values(n, seed=seed) if pairs else None
+        ks.copy_(dev(kh))
+        if pairs:
+            vs.copy_(dev(vh))
+        g.replay()
+        torch.cuda.synchronize()
+        if what == "ms_pairs_256":
+            ek, ev, eo = oracle.multisplit(kh, ob, vh)
+            assert np.array_equal(host(off), eo)
+        else:
+            ek, ev = oracle.radix_sort(kh, vh)
+        assert np.array_equal(host(ko), ek)
+        if pairs:
+            assert np.array_equal(host(vo), ev)
