@@ -101,3 +101,44 @@ def test_sort_pairs_beyond_2p31():
         seen[vs] = 1
         prev_k, prev_v = int(ks[-1]), int(vs[-1])
     assert bool(seen.all())
+
+
+@pytest.mark.parametrize("n", [(1 << 30) - 1, 1 << 30])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_sort_at_the_one_pass_limit(n, pairs):
+    """The one-pass sort's look-back words hold 30-bit prefixes: n = 2^30 - 1 is its largest
+    input, n = 2^30 takes the per-digit multisplit; both sort stably (checked on device)."""
+    k = torch.empty(n, dtype=torch.int32, device="cuda")
+    gdev.keys_(k, 11 + n % 7)
+    k[::3] &= 0xFF00FF  # duplicates: stability visible
+    v = torch.empty(n, dtype=torch.int32, device="cuda")
+    gdev.values_(v, 1, parity=True)  # v_i = i
+    if pairs:
+        ko, vo = ms.radix_sort(k, v, bits_per_pass=8)
+    else:
+        ko, _ = ms.radix_sort(k, None, bits_per_pass=8)
+        vo = None
+    torch.cuda.synchronize()
+    seen = torch.zeros(n, dtype=torch.uint8, device="cuda") if pairs else None
+    hist_in = torch.zeros(1 << 16, dtype=torch.int64, device="cuda")
+    hist_out = torch.zeros(1 << 16, dtype=torch.int64, device="cuda")
+    prev_k, prev_v = -1, -1
+    for s in range(0, n, CH):
+        e = min(n, s + CH)
+        ks = u64(ko[s:e])
+        assert bool((ks[1:] >= ks[:-1]).all()) and int(ks[0]) >= prev_k, "sorted"
+        hist_in += torch.bincount(u64(k[s:e]) >> 16, minlength=1 << 16)
+        hist_out += torch.bincount(ks >> 16, minlength=1 << 16)
+        if pairs:
+            vs = u64(vo[s:e])
+            same = ks[1:] == ks[:-1]
+            assert bool((vs[1:][same] > vs[:-1][same]).all()), "stable"
+            if int(ks[0]) == prev_k:
+                assert int(vs[0]) > prev_v
+            assert bool((u64(k[vs]) == ks).all())
+            seen[vs] = 1
+            prev_v = int(vs[-1])
+        prev_k = int(ks[-1])
+    assert torch.equal(hist_in, hist_out), "the same multiset of keys"
+    if pairs:
+        assert bool(seen.all())
