@@ -111,7 +111,8 @@ int ms_lane_ordered_increment(void);
  *   MS_OPT_SORT:       MS_SORT_AUTO (default: the radix sort computes every
  *                      digit histogram in one read and runs one fused
  *                      look-back pass per digit, 36 B/key for 4 x 8 bits;
- *                      where n < 2^30, the probe held, <= 8 passes) or
+ *                      where n < 2^30, the probe held, every digit has
+ *                      >= 7 bits) or
  *                      MS_SORT_PASSES (every pass a full multisplit,
  *                      P:1613-1616, 48 B/key).
  * ms_set_option returns MS_ERR_INVALID_VALUE for an unknown option / value;

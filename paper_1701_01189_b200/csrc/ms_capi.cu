@@ -459,8 +459,8 @@ ms_status onesweep_multisplit(const Plan &pl, bool pairs, const uint32_t *ki, co
 // Sec.6.3: iterated multisplits over <= 256 buckets, here LSD over
 // the 8-bit digits of the bucket id (ms_large.cuh).  RADIX digits wider than 8
 // bits are two radix passes over the keys themselves.
-// Workspace: [hdr][inner multisplit ws][RADIX: keys (+vals) of pass 1 |
-//             else: b0 p0 b1 p1 b2 (+p2 for pairs), n words each]
+// Workspace: [hdr][inner multisplit / radix-sort ws][non-RADIX: b0 p0 b1 p1 b2
+//             (+p2 for pairs), n words each]
 struct LargeLayout {
   size_t inner, inner_bytes, x[6], total;
 };
@@ -470,8 +470,11 @@ LargeLayout large_layout(uint64_t n, uint32_t kind, bool pairs) {
   const bool radix = kind == MS_BUCKET_RADIX || kind == MS_BUCKET_IDENTITY;
   lo.inner = kHdrBytes;
   lo.inner_bytes = std::max(ms_multisplit_workspace_size(n, 256, 0), ms_multisplit_workspace_size(n, 256, 1));
+  // radix digits (and top-bit delta buckets) of the key itself: an LSD radix sort
+  // over the digit's bits (the one-pass pipeline where it applies)
+  lo.inner_bytes = std::max(lo.inner_bytes, ms_radix_sort_workspace_size(n, 1));
   size_t off = lo.inner + align_up(lo.inner_bytes);
-  const int arrays = radix ? (pairs ? 2 : 1) : (pairs ? 6 : 5);
+  const int arrays = radix ? 0 : (pairs ? 6 : 5);  // the radix passes keep their own ping-pong buffer
   for (int i = 0; i < arrays; ++i) {
     lo.x[i] = off;
     off += align_up(n * 4u);
@@ -484,6 +487,10 @@ ms_status multisplit_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint
                           uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
                           uint32_t *bucket_offsets, void *ws, size_t ws_bytes, void *stream,
                           bool pairs);
+
+ms_status radix_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                     uint32_t *vals_out, uint64_t n, uint32_t begin_bit, uint32_t end_bit,
+                     uint32_t r, void *ws, size_t ws_bytes, void *stream, bool pairs);
 
 ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                      uint32_t *vals_out, uint64_t n, const ms_bucket_fn *fn,
@@ -519,14 +526,12 @@ ms_status large_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
       k_domain_check<<<min((uint32_t)((n + 255u) / 256u), 148u * 8u), 256, 0, s>>>(keys_in, (uint32_t)n, m, hdr);
       if (counted(cudaGetLastError()) != cudaSuccess) return done(MS_ERR_CUDA);
     }
-    uint32_t *tk = (uint32_t *)(w + lo.x[0]), *tv = pairs ? (uint32_t *)(w + lo.x[1]) : nullptr;
-    const ms_bucket_fn a{MS_BUCKET_RADIX, 256u, 0u, sh, 8u, nullptr};
-    const ms_bucket_fn b{MS_BUCKET_RADIX, 1u << (bits - 8u), 0u, sh + 8u, bits - 8u, nullptr};
+    // two stable passes, the low 8 bits of the digit first (Sec.6.3 as an LSD sort
+    // by the bucket id, R30): the radix sort over bits [sh, sh + bits)
     ev(1);
-    ms_status st = multisplit_impl(keys_in, vals_in, tk, tv, n, &a, nullptr, inner, lo.inner_bytes, s, pairs);
-    if (st != MS_SUCCESS) return done(st);
     ev(2);
-    st = multisplit_impl(tk, tv, keys_out, vals_out, n, &b, nullptr, inner, lo.inner_bytes, s, pairs);
+    const ms_status st = radix_impl(keys_in, vals_in, keys_out, vals_out, n, sh, sh + bits, 8u, inner,
+                                    lo.inner_bytes, s, pairs);
     if (st != MS_SUCCESS) return done(st);
     if (bucket_offsets) {
       k_offsets_sorted<<<min((uint32_t)((n + 256u) / 256u), 148u * 8u), 256, 0, s>>>(
@@ -733,9 +738,17 @@ ms_status radix_impl(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t 
     ms_bytes = x > ms_bytes ? x : ms_bytes;
   }
   char *w = (char *)ws;
-  uint32_t nbins = 0;
-  for (int p = 0; p < passes; ++p) nbins += 1u << bits[p];
-  if (onesweep_ok(n) && passes <= (int)kKoMaxPasses && nbins <= kKoMaxBins &&
+  uint32_t nbins = 0, min_bits = 32;
+  for (int p = 0; p < passes; ++p) {
+    nbins += 1u << bits[p];
+    min_bits = bits[p] < min_bits ? bits[p] : min_bits;
+  }
+  // the one-pass kernel's per-tile cost is that of 256 buckets and its ranks
+  // serialize on shared counters when few buckets take all the keys: it wins
+  // only when every digit has >= 7 bits (measured: 4 x 8 bits 88 -> 92 Gkeys/s,
+  // but 6 x 5 + 2 bits 66 -> 54, and 8 + 2 bits (m = 1024 top-bit buckets)
+  // 130 -> 111)
+  if (onesweep_ok(n) && min_bits >= 7u && passes <= (int)kKoMaxPasses && nbins <= kKoMaxBins &&
       g_opt[MS_OPT_SORT].load(std::memory_order_relaxed) == MS_SORT_AUTO) {
     // f1: every digit histogram in one read (KOH), then one KO pass per digit
     cudaStream_t s = (cudaStream_t)stream;

@@ -65,7 +65,7 @@ def test_sort_sizes(n, pairs):
     check_sort(keys, gen.values(n, seed=n) if pairs else None)
 
 
-@pytest.mark.parametrize("args", [(0, 32, 8), (0, 32, 4), (0, 32, 5), (0, 32, 6), (0, 32, 7), (8, 24, 8),
+@pytest.mark.parametrize("args", [(0, 32, 8), (0, 32, 4), (0, 32, 5), (0, 32, 6), (0, 32, 7), (0, 28, 7), (4, 32, 7), (8, 24, 8),
                                   (3, 17, 6), (31, 32, 1), (0, 8, 8), (0, 16, 8), (5, 29, 3), (0, 32, 0)])
 @pytest.mark.parametrize("pairs", [False, True])
 def test_sort_schedules(args, pairs):
