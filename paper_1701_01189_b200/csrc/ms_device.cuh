@@ -110,7 +110,10 @@ __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketPara
 // It also builds the cell table: CAP >= 256 (m <= 256) 1024 cells of the top 10
 // bits (4 KB), smaller tables 128 cells (512 B); cell c = [A_c | A_{c+1} << 16]
 // with A_c = the number of splitters below c << cell_shift (A_cells = m - 1).
-#define MS_STAGE_SPLITTERS(bp_, CAP)                                            \
+#define MS_STAGE_SPLITTERS(bp_, CAP) MS_STAGE_SPLITTERS3(bp_, CAP, true)
+// CELLS = false: no cell table (a one-tile, latency-bound kernel: the table's
+// build would cost more than the searches it saves)
+#define MS_STAGE_SPLITTERS3(bp_, CAP, CELLS)                                    \
   if constexpr (KIND == kSplitters) {                                           \
     constexpr uint32_t ms_cb_ = (CAP) >= 256 ? 10u : 7u;                        \
     __shared__ uint32_t ms_s_spl[CAP];                                          \
@@ -118,7 +121,7 @@ __device__ __forceinline__ uint32_t splitter_bucket(uint32_t u, const BucketPara
     for (uint32_t i_ = threadIdx.x; i_ < (bp_).m1 && i_ < (CAP); i_ += blockDim.x) \
       ms_s_spl[i_] = __ldg((bp_).spl + i_);                                     \
     __syncthreads();                                                            \
-    if ((bp_).m1 <= (CAP)) {                                                    \
+    if ((CELLS) && (bp_).m1 <= (CAP)) {                                         \
       for (uint32_t c_ = threadIdx.x; c_ < (1u << ms_cb_); c_ += blockDim.x) {  \
         const uint64_t lo_ = (uint64_t)c_ << (32u - ms_cb_);                    \
         const uint64_t hi_ = (uint64_t)(c_ + 1u) << (32u - ms_cb_);             \

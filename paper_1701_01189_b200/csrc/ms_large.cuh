@@ -82,7 +82,7 @@ constexpr uint32_t kSmallMax = 4096;
 
 template <int KIND, bool PAIRS>
 __global__ void __launch_bounds__(kThreads) k_small(KfArgs a, BucketParams bp) {
-  MS_STAGE_SPLITTERS(bp, kMaxBuckets);
+  MS_STAGE_SPLITTERS3(bp, kMaxBuckets, false);
   constexpr uint32_t W = kWarps, PER = kSmallMax / W, ITEMS = PER / 32;
   __shared__ uint32_t cnt[W][kMaxBuckets];
   __shared__ uint32_t s_base[kMaxBuckets];
