@@ -248,6 +248,9 @@ __device__ unsigned long long ko_lbstat[4];  // windows, spins, -, -
 #ifndef KO_R
 #define KO_R 2  // look-back rows per round trip, scan threads (measured: 2-3 > 4 > 8; 1 is slower)
 #endif
+#ifndef KO_CH
+#define KO_CH 4  // scatter chunk, slots per thread per round (measured: 4 > 2, 8 > 1, 16)
+#endif
 #ifndef KO_RL
 #define KO_RL 2  // look-back rows per round trip, dedicated look-back warps
 #endif
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__((ko_warps(PAIRS) + ko_lb_warps(PAIRS)) * 32, 1
     const uint32_t *tab = s_tab + (it & 1u) * NB;
     const uint32_t tn = tile_n(t);
     const uint32_t s0 = warp * (ITEMS * 32u) + lane;
-    constexpr uint32_t CH = 8;
+    constexpr uint32_t CH = KO_CH;
 #pragma unroll
     for (uint32_t c = 0; c < ITEMS; c += CH) {
       uint32_t kk[CH], vv[PAIRS ? CH : 1], pos[CH];
